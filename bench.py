@@ -1,0 +1,342 @@
+"""SRJ solve benchmark (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on):
+2D Poisson, 5-point stencil, 2048 x 2048 interior, Dirichlet, f ~ U[-1,1) from
+SplitMix64(seed), x0 = 0, fp64, learned SRJ scheme selection (Heuristic 0.4/0.2)
+until the relative residual <= 1e-8.  One step = one full solve.
+
+  value     GLUP/s = points x sweeps / device time, inputs resident in HBM
+  e2e       the same metric through the public API `solve()` with pinned host
+            b/x0 in and x out (H2D + D2H inside the timed region)
+  roofline  algorithmic bytes of the cycle kernel (24 B per point-sweep + 16 B
+            per point for the end-of-cycle residual) / its event-timed duration
+            vs the measured HBM copy bandwidth (MEASURED_PEAKS.json)
+  cpu_baseline  the oracle port (oracle/srj_oracle.c, OpenMP) on a bounded
+            sample of the same workload on this host's cores
+
+`--impl reference` times the CPU port alone (the reference is pure Python and
+cannot travel to the GPU box; its restatement is the oracle, pinned bit-exact
+against it in tests/test_oracle.py).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG_DESC = {
+    "c2": "2D Poisson 5-pt 2048^2 Dirichlet, f~U[-1,1) SplitMix64, rel L2 1e-8, SRJ heuristic",
+    "c3": "3D Poisson 7-pt 512^3 Dirichlet, f~U[-1,1) SplitMix64, rel L2 1e-8, SRJ heuristic",
+    "c1": "1D Poisson 3-pt N=1024 Dirichlet, f~U[-1,1) SplitMix64, rel L2 1e-8, SRJ heuristic",
+    "c4": "2D var-coef 5-pt 4096^2 harmonic faces k=exp(g), rel L2 1e-8, SRJ heuristic",
+}
+BYTES_PER_UPDATE = {"1d3": 24, "2d5": 24, "3d7": 24, "2d5var": 40}
+L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIG_DESC))
+    ap.add_argument("--size", type=int, default=None, help="override the grid extent")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--sweeps-per-pass", type=int, default=None)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) == 7:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()),
+                 default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[3 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def traffic_from_profile(config):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(config)
+    except Exception:
+        return None
+
+
+def cpu_sample(family, n, seed, budget_s):
+    """Bounded CPU sample: SRJ sweeps (update + residual + norm, the reference's
+    per-sweep work) with the OpenMP oracle port on this host's cores."""
+    import numpy as np
+
+    from oracle import srj_oracle as O
+    op = O.stencil(family, n)
+    b = O.uniform_rhs(seed, op.n)
+    seq = O.scheme(O.LADDER[14])[0]
+    x = np.zeros(op.n)
+    r, s = op.residual(x, b)
+    sweeps = 0
+    t0 = time.perf_counter()
+    while True:
+        x = op.update(x, r, seq[sweeps % len(seq)])
+        r, s = op.residual(x, b)
+        sweeps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    return {"value": op.n * sweeps / el / 1e9, "unit": "GLUP/s", "cores": O.clib().oracle_threads(),
+            "kind": "port",
+            "sample": f"{sweeps} SRJ sweeps (update+residual+norm) of the {family} n={n} grid, "
+                      f"{el:.1f} s, oracle/srj_oracle.c OpenMP"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2011_06636_b200.problems import CONFIGS
+    family, extent, _ = CONFIGS[args.config]
+    n = args.size or extent
+    for _ in range(args.warmup):
+        cpu_sample(family, n, args.seed, min(2.0, args.cpu_seconds))
+    vals = []
+    samples = []
+    for _ in range(args.steps):
+        c = cpu_sample(family, n, args.seed, args.cpu_seconds / max(args.steps, 1))
+        vals.append(c["value"])
+        samples.append(c)
+    v = sum(vals) / len(vals)
+    npts = {"1d3": n, "2d5": n * n, "2d5var": n * n, "3d7": n ** 3}[family]
+    line = {
+        "impl": "reference", "metric": "GLUP/s (SRJ point-updates/s)", "value": v,
+        "unit": "GLUP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (SplitMix64 f, seeded)",
+        "config": {"workload": CONFIG_DESC[args.config], "n": npts, "grid": n},
+        "cpu_baseline": {"value": v, "unit": "GLUP/s", "cores": samples[-1]["cores"],
+                         "kind": "port", "sample": samples[-1]["sample"]},
+        "e2e": {"value": v, "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2011_06636_b200 as srj
+    from paper_2011_06636_b200.problems import CONFIGS
+    from paper_2011_06636_b200.solver import solve_fields
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    family, extent, _ = CONFIGS[args.config]
+    n = args.size or extent
+    prob = srj.baseline_problem(family, n, seed=args.seed, device=dev, rhs_on_device=True)
+    A = prob.A
+    if args.sweeps_per_pass:
+        A.set_sweeps_per_pass(args.sweeps_per_pass)
+    b = A.field(prob.b)
+    x = A.new_field()
+    x_alt = A.new_field()
+    rule = srj.StoppingRule("relative_l2", args.tol, 10**9)
+    ctrl = srj.Heuristic()
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    launch_ms = []
+    launch_bytes = []
+    bpu = BYTES_PER_UPDATE[family]
+
+    def one_solve():
+        x.buf.zero_()
+        return solve_fields(A, b, x, x_alt, ctrl, rule, record_history=False)
+
+    # warm-up (also builds every scheme the solve visits)
+    rep = None
+    for _ in range(args.warmup):
+        rep = one_solve()
+    torch.cuda.synchronize()
+
+    # per-launch timing of the cycle kernel: time each srj_run_cycle with events
+    from paper_2011_06636_b200 import operators as ops_mod
+    orig_run_cycle = ops_mod.StencilOperator.run_cycle
+
+    def timed_run_cycle(self, *a, **kw):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out = orig_run_cycle(self, *a, **kw)
+        e1.record(stream)
+        e1.synchronize()
+        if out.executed > 0:
+            launch_ms.append(e0.elapsed_time(e1))
+            launch_bytes.append(bpu * A.n * out.executed + 16 * A.n)
+        return out
+
+    ops_mod.StencilOperator.run_cycle = timed_run_cycle
+
+    step_ms = []
+    sweeps = []
+    launches = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.fill_(1.0)   # evict b/x from L2 between steps
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rep = one_solve()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            sweeps.append(rep.total_iterations)
+            launches += len(rep.cycles) + 2  # cycle kernels + baseline/first residual
+        torch.cuda.synchronize()
+    ops_mod.StencilOperator.run_cycle = orig_run_cycle
+    if world > 1:
+        dist.barrier()
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    updates = A.n * sum(sweeps) * world
+    value = updates / (total_ms * 1e-3) / 1e9
+
+    # e2e: public API with pinned host buffers, H2D + D2H inside the region
+    b_host = torch.empty(A.n, dtype=torch.float64, pin_memory=True)
+    b_host.copy_(prob.b)
+    x0_host = torch.zeros(A.n, dtype=torch.float64, pin_memory=True)
+    p_host = srj.ProblemInstance(A=A, b=b_host, x0=x0_host, stopping_norm="relative_l2")
+    e2e_ms = []
+    e2e_sweeps = []
+    for _ in range(max(1, min(args.steps, 3))):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r2 = srj.solve(p_host, ctrl, rule, record_history=False)
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e_sweeps.append(r2.total_iterations)
+        assert r2.total_iterations == rep.total_iterations
+    e2e_val = A.n * sum(e2e_sweeps) / (sum(e2e_ms) * 1e-3) / 1e9
+
+    peak, peak_kind = measured_peak()
+    achieved = sum(launch_bytes) / (sum(launch_ms) * 1e-3) / 1e9 if launch_ms else None
+    traffic = traffic_from_profile(args.config)
+    line = {
+        "metric": "GLUP/s (SRJ point-updates/s); time-to-rel-residual 1e-8",
+        "value": value, "unit": "GLUP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (f = 2u-1, u from SplitMix64(seed) in index order; x0 = 0)",
+        "config": {"workload": CONFIG_DESC[args.config], "grid": n, "n": A.n,
+                   "sweeps_per_solve": sweeps[-1], "cycles_per_solve": len(rep.cycles),
+                   "levels_tail": [c.level for c in rep.cycles][-6:],
+                   "time_to_tolerance_ms": ms_per_step,
+                   "l2": "flushed between steps (512 MiB write)",
+                   "sweeps_per_pass": args.sweeps_per_pass or 1,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "e2e": {"value": e2e_val, "unit": "GLUP/s",
+                "h2d_bytes_per_step": 2 * 8 * A.n, "d2h_bytes_per_step": 8 * A.n,
+                "ms_per_step": sum(e2e_ms) / len(e2e_ms)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None, "traffic": traffic,
+                     "peak_kind": peak_kind, "kernel": "srj::k_cycle",
+                     "bytes_per_update": bpu,
+                     "launches_timed": len(launch_ms)},
+        "clocks": clocks.summary(),
+        "gpu_launches": launches,
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_sample(family, n, args.seed, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

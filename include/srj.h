@@ -1,0 +1,144 @@
+/*
+ * srj.h -- C ABI of libsrj.so, the sm_100a device path of the Scheduled
+ * Relaxation Jacobi (SRJ) solve (arXiv 2011.06636).
+ *
+ * The reference (pure Python, /root/reference/pkg/src/srj) has no FFI: its hot
+ * path is the duck-typed operator surface `run_cycle` touches.  Each entry
+ * point below names the reference code it replaces:
+ *
+ *   srj_run_cycle      solver.run_cycle's sweep loop            solver.py:216-243
+ *                      + the post-loop convergence test          solver.py:245-249
+ *                      (x + w*(inv_diag*r), b - csr.dot(x), np.linalg.norm,
+ *                       np.isfinite, per-sweep tol/budget tests, history)
+ *   srj_residual_sq    b - A.scipy_csr().dot(x) and its squared norm, used for
+ *                      the relative baseline and a cold cycle start
+ *                                                                solver.py:209-210,300-304
+ *   srj_sweep          sparse.weighted_jacobi_sweep              sparse.py:84-93
+ *   srj_matvec         sparse.matvec / csr_matvec                sparse.py:78-81
+ *   srj_fill_uniform_rhs  f_i = 2*SplitMix64(seed).uniform()-1 in index order
+ *                      (rng.py:25-40; idiom of problems.py:382)
+ *   srj_op_create      sparse.SparseMatrix construction for the structured
+ *                      Dirichlet stencils (problems.py:50-69, 148-177)
+ *
+ * Conventions
+ *   - Status codes: SRJ_OK, SRJ_DIVERGED, SRJ_BAD_ARGUMENT, SRJ_CUDA_ERROR;
+ *     srj_last_error() returns a thread-local message for the last failure.
+ *   - All vectors are caller-owned fp64 device buffers (torch tensors' data_ptr()).
+ *     Every x / x_alt / b pointer addresses the FIRST INTERIOR point of a buffer
+ *     that also holds `halo` ghost elements before and after the n interior points
+ *     (halo = one plane: 1 in 1D, nx in 2D, nx*ny in 3D; see srj_op_layout).
+ *     Ghost values are read, never written: zero for a Dirichlet side, the
+ *     neighbour slab's boundary plane for an internal slab side.
+ *   - Work is stream-ordered on `stream` (a cudaStream_t, NULL = legacy default).
+ *     srj_run_cycle and srj_residual_sq synchronise the stream once before they
+ *     return (the host reads one small result struct per cycle); the other
+ *     calls are asynchronous.
+ *   - No allocation inside a cycle: all scratch is owned by the srj_op handle.
+ *     Handles are independent and may be used from different threads; one
+ *     handle must not be used concurrently.
+ *   - Iterates are bit-identical to the reference CSR path: every stencil sum is
+ *     a left-to-right, separately rounded sum over ascending CSR columns and the
+ *     update is t = inv_diag*r; t = w*t; x' = x + t (no FMA contraction).
+ *     Residual norms are deterministic (fixed-order reductions) but are summed in
+ *     a different order than OpenBLAS ddot, so they agree to ~1e-15 relative.
+ */
+#ifndef SRJ_H
+#define SRJ_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SRJ_ABI_VERSION 1
+
+enum srj_status {
+    SRJ_OK = 0,
+    SRJ_DIVERGED = 1,      /* a residual or iterate became non-finite */
+    SRJ_BAD_ARGUMENT = 2,
+    SRJ_CUDA_ERROR = 3
+};
+
+enum srj_family {
+    SRJ_STENCIL_1D3 = 1,     /* 1D 3-point, (-1, 2, -1)*dx2                 */
+    SRJ_STENCIL_2D5 = 2,     /* 2D 5-point, (-1,-1, 4,-1,-1)*dx2            */
+    SRJ_STENCIL_3D7 = 3,     /* 3D 7-point, 6*dx2 diagonal, -dx2 neighbours  */
+    SRJ_STENCIL_2D5_VAR = 4  /* 2D 5-point, harmonic-mean face coefficients  */
+};
+
+/* Outcome of one cycle; mirrors the reference's CycleStats plus the buffer
+ * that holds the final iterate. */
+enum srj_cycle_status {
+    SRJ_CYCLE_RAN = 0,        /* all sweeps applied (or budget cut), tol not met */
+    SRJ_CYCLE_CONVERGED = 1,  /* stopping rule met (mid-cycle or after last sweep) */
+    SRJ_CYCLE_DIVERGED = 2    /* non-finite residual after sweep `executed`        */
+};
+
+typedef struct srj_op srj_op;
+
+typedef struct srj_op_desc {
+    int32_t family;        /* enum srj_family */
+    int32_t device;        /* CUDA ordinal the buffers live on */
+    int64_t nx, ny, nz;    /* interior extents of THIS operator's grid (slab); unused axes = 1 */
+    double  dx2;           /* constant coefficient scale (N+1)^2 (ignored for *_VAR) */
+    /* *_VAR only: face coefficients already scaled by dx2, device pointers.
+     * face_x: ny rows of nx+1 faces (face i sits between points i-1 and i);
+     * face_y: ny+1 rows of nx faces (row j sits between rows j-1 and j). */
+    const double* face_x;
+    const double* face_y;
+} srj_op_desc;
+
+typedef struct srj_cycle_out {
+    int32_t executed;       /* sweeps applied (CycleStats.executed) */
+    int32_t status;         /* enum srj_cycle_status */
+    int32_t result_in_alt;  /* 1: final iterate is in x_alt; 0: in x */
+    int32_t launches;       /* kernel launches used by the cycle (diagnostic) */
+    double  res_before;     /* CycleStats.residual_before */
+    double  res_after;      /* CycleStats.residual_after  */
+} srj_cycle_out;
+
+int srj_abi_version(void);
+const char* srj_last_error(void);
+
+int srj_op_create(const srj_op_desc* desc, srj_op** out);
+int srj_op_destroy(srj_op* op);
+/* n interior points and the ghost elements required before/after them. */
+int srj_op_layout(const srj_op* op, int64_t* n, int64_t* halo);
+/* Diagonal value and its reciprocal for constant-coefficient families
+ * (diag = 2d*dx2, inv = 1/diag as the reference's SparseMatrix caches it). */
+int srj_op_diag(const srj_op* op, double* diag, double* inv_diag);
+/* Temporal blocking: sweeps fused per HBM pass (1 = one sweep per pass). */
+int srj_op_set_sweeps_per_pass(srj_op* op, int32_t s);
+
+/* sum_i (b - A x)_i^2 -> *sumsq_host.  Synchronises `stream`. */
+int srj_residual_sq(srj_op* op, const double* x, const double* b,
+                    double* sumsq_host, void* stream);
+
+/* One SRJ cycle of up to min(M, budget) sweeps with omegas_dev[k] applied by
+ * sweep k (device array, application order).  Before sweep k >= 1 the cycle
+ * stops when ||b - A x_k|| / baseline <= tol or is non-finite; res_before is the
+ * residual of the incoming x (the host already knows it).  x and x_alt are
+ * ping-pong buffers (both with ghosts); x is overwritten, the final iterate is
+ * in x (result_in_alt == 0) or x_alt.  history_host, if non-NULL, receives the
+ * relative residual after each executed sweep (executed entries).
+ * Returns SRJ_OK also for a diverged cycle (out->status says so). */
+int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
+                  const double* omegas_dev, int32_t M, double tol, double baseline,
+                  double res_before, int64_t budget, double* history_host,
+                  srj_cycle_out* out, void* stream);
+
+/* x_out = x + omega * inv_diag * (b - A x)  (one weighted Jacobi sweep). */
+int srj_sweep(srj_op* op, const double* x, double* x_out, const double* b,
+              double omega, void* stream);
+/* y = A x (y needs no ghosts). */
+int srj_matvec(srj_op* op, const double* x, double* y, void* stream);
+/* out[i] = 2 * u_{start+i} - 1, u_j the j-th uniform of SplitMix64(seed). */
+int srj_fill_uniform_rhs(double* out, int64_t n, uint64_t seed, int64_t start,
+                         int32_t device, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SRJ_H */

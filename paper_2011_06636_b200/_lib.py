@@ -1,0 +1,98 @@
+"""ctypes binding of libsrj.so (the C ABI in include/srj.h).
+
+The library is the only compute path: importing the package works without it
+(host-side scheme construction, problem metadata), but every device call goes
+through `lib()`, which raises if the shared object is missing or was built
+against a different ABI.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_double, c_int32, c_int64, c_uint64, c_void_p
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsrj.so")
+ABI_VERSION = 1
+
+SRJ_OK, SRJ_DIVERGED, SRJ_BAD_ARGUMENT, SRJ_CUDA_ERROR = 0, 1, 2, 3
+SRJ_STENCIL_1D3, SRJ_STENCIL_2D5, SRJ_STENCIL_3D7, SRJ_STENCIL_2D5_VAR = 1, 2, 3, 4
+CYCLE_RAN, CYCLE_CONVERGED, CYCLE_DIVERGED = 0, 1, 2
+
+# Every symbol include/srj.h declares (checked by tests/test_abi.py).
+EXPORTED_SYMBOLS = (
+    "srj_abi_version", "srj_last_error", "srj_op_create", "srj_op_destroy",
+    "srj_op_layout", "srj_op_diag", "srj_op_set_sweeps_per_pass", "srj_residual_sq",
+    "srj_run_cycle", "srj_sweep", "srj_matvec", "srj_fill_uniform_rhs",
+)
+
+
+class OpDesc(ctypes.Structure):
+    _fields_ = [
+        ("family", c_int32), ("device", c_int32),
+        ("nx", c_int64), ("ny", c_int64), ("nz", c_int64),
+        ("dx2", c_double),
+        ("face_x", c_void_p), ("face_y", c_void_p),
+    ]
+
+
+class CycleOut(ctypes.Structure):
+    _fields_ = [
+        ("executed", c_int32), ("status", c_int32), ("result_in_alt", c_int32),
+        ("launches", c_int32), ("res_before", c_double), ("res_after", c_double),
+    ]
+
+
+class SrjLibraryError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def _declare(L):
+    L.srj_abi_version.restype = c_int32
+    L.srj_last_error.restype = ctypes.c_char_p
+    L.srj_op_create.argtypes = [POINTER(OpDesc), POINTER(c_void_p)]
+    L.srj_op_destroy.argtypes = [c_void_p]
+    L.srj_op_layout.argtypes = [c_void_p, POINTER(c_int64), POINTER(c_int64)]
+    L.srj_op_diag.argtypes = [c_void_p, POINTER(c_double), POINTER(c_double)]
+    L.srj_op_set_sweeps_per_pass.argtypes = [c_void_p, c_int32]
+    L.srj_residual_sq.argtypes = [c_void_p, c_void_p, c_void_p, POINTER(c_double), c_void_p]
+    L.srj_run_cycle.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
+                                c_double, c_double, c_double, c_int64, c_void_p,
+                                POINTER(CycleOut), c_void_p]
+    L.srj_sweep.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_void_p]
+    L.srj_matvec.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p]
+    L.srj_fill_uniform_rhs.argtypes = [c_void_p, c_int64, c_uint64, c_int64, c_int32, c_void_p]
+    for name in EXPORTED_SYMBOLS:
+        if name not in ("srj_abi_version", "srj_last_error"):
+            getattr(L, name).restype = c_int32
+
+
+def load(path: str = LIB_PATH):
+    """Load and type the shared library (no CUDA call is made)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise SrjLibraryError(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (there is no CPU fallback)")
+    L = ctypes.CDLL(path)
+    _declare(L)
+    if L.srj_abi_version() != ABI_VERSION:
+        raise SrjLibraryError(f"libsrj ABI {L.srj_abi_version()} != expected {ABI_VERSION}")
+    _lib = L
+    return L
+
+
+def lib():
+    return load()
+
+
+def check(rc: int, what: str) -> None:
+    if rc != SRJ_OK:
+        msg = lib().srj_last_error().decode(errors="replace")
+        raise SrjLibraryError(f"{what} failed (status {rc}): {msg}")

@@ -1,0 +1,458 @@
+// libsrj.so: sm_100a SRJ sweep kernels and the C ABI declared in include/srj.h.
+//
+// Cycle execution model (one launch per cycle):
+//   a persistent cooperative kernel holds one CTA per resident slot on every SM
+//   and walks the M sweeps of the cycle itself.  Each sweep reads x_k (ping-pong
+//   buffer), writes x_{k+1} and accumulates the squared residual r_k = b - A x_k
+//   of its INPUT iterate; after a grid barrier every CTA reduces the per-CTA
+//   partials in the same fixed order (bit-identical in all CTAs), so all CTAs
+//   agree on res_k = sqrt(sum r_k^2)/baseline without another barrier and stop
+//   together before sweep k when res_k <= tol or is non-finite -- the
+//   reference's per-sweep stopping rule (solver.py:216-222,235-239).  Because the
+//   residual of x_k is produced by the sweep that consumes x_k, x_k is still
+//   intact in the input buffer when the cycle stops there.  After the last sweep
+//   a residual-only pass gives res(x_M) (solver.py:233-234,248-249).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/srj.h"
+#include "srj_common.cuh"
+#include "srj_stencil.cuh"
+#include "srj_tb.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace srj {
+
+constexpr int kMaxSchemeLength = 10000;  // reference schemes.py:24
+constexpr int kThreads = 256;
+constexpr int kSmallThreads = 1024;
+constexpr long long kSmallUnits = 256;   // <= 8192 points: one CTA, no grid barrier
+
+enum Mode { kSweep = 0, kResid = 1, kMatvec = 2 };
+
+// Walk the 32-point x-row units [u0, u1): warps take units round-robin so a
+// CTA's warps stream through consecutive rows together (coalesced rows, and
+// the y/z neighbour rows are reused from L1/L2 while still hot).
+template <int FAM, int MODE>
+__device__ __forceinline__ double walk_units(const Geom& g, const double* x, double* out,
+                                             const double* __restrict__ b, double w,
+                                             int u0, int u1) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double acc = 0.0;
+    for (int u = u0 + warp; u < u1; u += nw) {
+        const int row = u / g.upr;
+        const int i = (u - row * g.upr) * 32 + lane;
+        if (i < g.nx) {
+            const int j = (FAM == F3D) ? row % g.ny : row;
+            const long long k = (long long)row * g.nx + i;
+            double xc, inv;
+            const double y = apply_at<FAM>(g, x, k, i, j, xc, inv);
+            if constexpr (MODE == kMatvec) {
+                out[k] = y;
+            } else {
+                const double r = DSUB(__ldg(b + k), y);
+                acc = fma(r, r, acc);
+                if constexpr (MODE == kSweep) out[k] = relax(xc, inv, r, w);
+            }
+        }
+    }
+    return acc;
+}
+
+struct CycleArgs {
+    Geom g;
+    const double* xa;      // x_0 (also receives x_2, x_4, ...)
+    double* xb;            // receives x_1, x_3, ...
+    const double* b;
+    const double* omegas;  // application order
+    int M;                 // sweeps allowed this cycle (0: residual only)
+    double tol, baseline;
+    double* partials;      // [2][gridDim.x]
+    double* hist;          // [M+1] relative residual of x_k
+    int* out_i;            // executed, status
+    double* out_d;         // final sum of squares, res_after
+};
+
+__device__ __forceinline__ void grid_barrier() {
+    if (gridDim.x == 1) {
+        __syncthreads();
+    } else {
+        cg::this_grid().sync();
+    }
+}
+
+template <int FAM>
+__global__ void __launch_bounds__(1024) k_cycle(CycleArgs a) {
+    __shared__ double sh[32];
+    const int nb = gridDim.x;
+    const int u0 = (int)((long long)a.g.units * blockIdx.x / nb);
+    const int u1 = (int)((long long)a.g.units * (blockIdx.x + 1) / nb);
+    double* const buf[2] = {const_cast<double*>(a.xa), a.xb};
+    int executed = a.M, status = kStatusRan;
+    double S = 0.0, res = 0.0;
+    for (int k = 0; k <= a.M; ++k) {
+        const bool tail = (k == a.M);
+        const double* xin = buf[k & 1];
+        double acc = tail ? walk_units<FAM, kResid>(a.g, xin, nullptr, a.b, 0.0, u0, u1)
+                          : walk_units<FAM, kSweep>(a.g, xin, buf[(k + 1) & 1], a.b, a.omegas[k], u0, u1);
+        double* part = a.partials + (k & 1) * nb;
+        acc = block_allsum(acc, sh);
+        if (threadIdx.x == 0) part[blockIdx.x] = acc;
+        grid_barrier();
+        if (k >= 1 || tail) {
+            double s = 0.0;
+            for (int q = threadIdx.x; q < nb; q += blockDim.x) s += __ldcg(part + q);
+            S = block_allsum(s, sh);
+            res = sqrt(S) / a.baseline;
+            if (k >= 1) {
+                if (blockIdx.x == 0 && threadIdx.x == 0) a.hist[k] = res;
+                if (!isfinite(res)) { executed = k; status = kStatusDiverged; break; }
+                if (res <= a.tol) { executed = k; status = kStatusConverged; break; }
+            }
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.out_i[0] = executed;
+        a.out_i[1] = status;
+        a.out_i[2] = executed & 1;  // x_executed lives in buf[executed & 1]
+        a.out_d[0] = S;
+        a.out_d[1] = res;
+    }
+}
+
+template <int FAM, int MODE>
+__global__ void __launch_bounds__(kThreads) k_apply(Geom g, const double* x, double* out,
+                                                    const double* __restrict__ b, double w) {
+    const int nb = gridDim.x;
+    const int u0 = (int)((long long)g.units * blockIdx.x / nb);
+    const int u1 = (int)((long long)g.units * (blockIdx.x + 1) / nb);
+    walk_units<FAM, MODE>(g, x, out, b, w, u0, u1);
+}
+
+// SplitMix64 counter form: draw i of a stream seeded with s is
+// mix(s + (i+1)*GAMMA) (reference rng.py:25-40), f = 2u - 1.
+__global__ void k_fill_rhs(double* out, long long n, unsigned long long seed, long long start) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        unsigned long long z = seed + (unsigned long long)(start + i + 1) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const double u = (double)(z >> 11) * 0x1.0p-53;
+        out[i] = DSUB(DMUL(2.0, u), 1.0);
+    }
+}
+
+}  // namespace srj
+
+using namespace srj;
+
+// ----------------------------------------------------------------------------
+// Host side
+// ----------------------------------------------------------------------------
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+    do {                                                                                 \
+        cudaError_t _e = (expr);                                                         \
+        if (_e != cudaSuccess)                                                           \
+            return fail(SRJ_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+struct srj_op {
+    srj_op_desc desc;
+    Geom g;
+    int device = 0;
+    int num_sms = 0;
+    int coop_blocks = 0;     // cooperative grid of the cycle kernel
+    int coop_threads = 0;
+    int sweeps_per_pass = 1;
+    double* partials = nullptr;  // device scratch
+    double* hist = nullptr;      // device [kMaxSchemeLength + 2]
+    int* out_i = nullptr;        // device [4]
+    double* out_d = nullptr;     // device [4]
+    int* h_out_i = nullptr;      // pinned mirrors
+    double* h_out_d = nullptr;
+    double* h_hist = nullptr;
+    TbPlan tb;                   // temporal-blocking plan (srj_tb.cuh)
+};
+
+template <int FAM>
+static const void* cycle_kernel() { return (const void*)&k_cycle<FAM>; }
+
+static const void* cycle_kernel_for(int fam) {
+    switch (fam) {
+        case F1D: return cycle_kernel<F1D>();
+        case F2D: return cycle_kernel<F2D>();
+        case F3D: return cycle_kernel<F3D>();
+        default: return cycle_kernel<F2DV>();
+    }
+}
+
+template <int MODE>
+static int launch_apply(srj_op* op, const double* x, double* out, const double* b, double w,
+                        cudaStream_t st) {
+    const int blocks = (int)std::max<long long>(1, std::min<long long>((op->g.units + 7) / 8, 16ll * op->num_sms));
+    switch (op->g.fam) {
+        case F1D: k_apply<F1D, MODE><<<blocks, kThreads, 0, st>>>(op->g, x, out, b, w); break;
+        case F2D: k_apply<F2D, MODE><<<blocks, kThreads, 0, st>>>(op->g, x, out, b, w); break;
+        case F3D: k_apply<F3D, MODE><<<blocks, kThreads, 0, st>>>(op->g, x, out, b, w); break;
+        default: k_apply<F2DV, MODE><<<blocks, kThreads, 0, st>>>(op->g, x, out, b, w); break;
+    }
+    CUDA_TRY(cudaGetLastError());
+    return SRJ_OK;
+}
+
+extern "C" {
+
+int srj_abi_version(void) { return SRJ_ABI_VERSION; }
+
+const char* srj_last_error(void) { return g_last_error.c_str(); }
+
+int srj_op_create(const srj_op_desc* d, srj_op** out) {
+    if (!d || !out) return fail(SRJ_BAD_ARGUMENT, "null argument");
+    *out = nullptr;
+    if (d->family < SRJ_STENCIL_1D3 || d->family > SRJ_STENCIL_2D5_VAR)
+        return fail(SRJ_BAD_ARGUMENT, "unknown stencil family");
+    if (d->nx < 1 || d->ny < 1 || d->nz < 1)
+        return fail(SRJ_BAD_ARGUMENT, "extents must be positive");
+    const bool var = d->family == SRJ_STENCIL_2D5_VAR;
+    if (var && (!d->face_x || !d->face_y))
+        return fail(SRJ_BAD_ARGUMENT, "variable-coefficient operator needs face_x and face_y");
+    if (!var && !(d->dx2 > 0.0))
+        return fail(SRJ_BAD_ARGUMENT, "dx2 must be positive");
+    if (d->family == SRJ_STENCIL_1D3 && (d->ny != 1 || d->nz != 1))
+        return fail(SRJ_BAD_ARGUMENT, "1D operator needs ny == nz == 1");
+    if ((d->family == SRJ_STENCIL_2D5 || var) && d->nz != 1)
+        return fail(SRJ_BAD_ARGUMENT, "2D operator needs nz == 1");
+    const long long rows = d->ny * d->nz;
+    const long long upr = (d->nx + 31) / 32;
+    if (d->nx >= (1ll << 31) || rows * upr >= (1ll << 31))
+        return fail(SRJ_BAD_ARGUMENT, "grid too large for one operator (shard it into slabs)");
+
+    DeviceGuard guard(d->device);
+    srj_op* op = new srj_op();
+    op->desc = *d;
+    op->device = d->device;
+    Geom& g = op->g;
+    g.fam = d->family;
+    g.nx = (int)d->nx;
+    g.ny = (int)d->ny;
+    g.nz = (int)d->nz;
+    g.n = d->nx * d->ny * d->nz;
+    g.plane = d->family == SRJ_STENCIL_1D3 ? 1 : (d->family == SRJ_STENCIL_3D7 ? d->nx * d->ny : d->nx);
+    g.rows = (int)rows;
+    g.upr = (int)upr;
+    g.units = (int)(rows * upr);
+    const double dim = d->family == SRJ_STENCIL_1D3 ? 1.0 : (d->family == SRJ_STENCIL_3D7 ? 3.0 : 2.0);
+    g.c_off = -1.0 * d->dx2;                  // reference problems.py:59,170
+    g.c_diag = (2.0 * dim) * d->dx2;          // 2*dx2, 4*dx2, 6*dx2 (problems.py:58,164)
+    g.inv_diag = 1.0 / g.c_diag;              // sparse.py:44
+    g.fx = d->face_x;
+    g.fy = d->face_y;
+
+    cudaDeviceProp prop;
+    cudaError_t e = cudaGetDeviceProperties(&prop, d->device);
+    if (e != cudaSuccess) { delete op; return fail(SRJ_CUDA_ERROR, cudaGetErrorString(e)); }
+    op->num_sms = prop.multiProcessorCount;
+    if (!prop.cooperativeLaunch) { delete op; return fail(SRJ_CUDA_ERROR, "device lacks cooperative launch"); }
+
+    if (g.units <= kSmallUnits) {
+        op->coop_blocks = 1;
+        op->coop_threads = kSmallThreads;
+    } else {
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cycle_kernel_for(g.fam), kThreads, 0);
+        if (e != cudaSuccess || per_sm < 1) { delete op; return fail(SRJ_CUDA_ERROR, "occupancy query failed"); }
+        long long want = (long long)per_sm * op->num_sms;
+        // at least ~4 units per warp keeps the per-sweep reduction cheap
+        const long long cap = std::max<long long>(1, g.units / (4 * (kThreads / 32)));
+        op->coop_blocks = (int)std::min(want, cap);
+        op->coop_threads = kThreads;
+    }
+    const size_t nparts = 2 * (size_t)std::max(op->coop_blocks, 8 * op->num_sms) * kTbMaxSub;
+    if ((e = cudaMalloc(&op->partials, nparts * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&op->hist, (kMaxSchemeLength + 2) * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&op->out_i, 4 * sizeof(int))) != cudaSuccess ||
+        (e = cudaMalloc(&op->out_d, 4 * sizeof(double))) != cudaSuccess ||
+        (e = cudaHostAlloc(&op->h_out_i, 4 * sizeof(int), cudaHostAllocDefault)) != cudaSuccess ||
+        (e = cudaHostAlloc(&op->h_out_d, 4 * sizeof(double), cudaHostAllocDefault)) != cudaSuccess ||
+        (e = cudaHostAlloc(&op->h_hist, (kMaxSchemeLength + 2) * sizeof(double), cudaHostAllocDefault)) != cudaSuccess) {
+        srj_op_destroy(op);
+        return fail(SRJ_CUDA_ERROR, std::string("allocation failed: ") + cudaGetErrorString(e));
+    }
+    tb_plan_init(op->tb, g, op->num_sms);
+    *out = op;
+    return SRJ_OK;
+}
+
+int srj_op_destroy(srj_op* op) {
+    if (!op) return SRJ_OK;
+    DeviceGuard guard(op->device);
+    cudaFree(op->partials);
+    cudaFree(op->hist);
+    cudaFree(op->out_i);
+    cudaFree(op->out_d);
+    cudaFreeHost(op->h_out_i);
+    cudaFreeHost(op->h_out_d);
+    cudaFreeHost(op->h_hist);
+    delete op;
+    return SRJ_OK;
+}
+
+int srj_op_layout(const srj_op* op, int64_t* n, int64_t* halo) {
+    if (!op) return fail(SRJ_BAD_ARGUMENT, "null operator");
+    if (n) *n = op->g.n;
+    if (halo) *halo = op->g.plane;
+    return SRJ_OK;
+}
+
+int srj_op_diag(const srj_op* op, double* diag, double* inv_diag) {
+    if (!op) return fail(SRJ_BAD_ARGUMENT, "null operator");
+    if (op->g.fam == F2DV) return fail(SRJ_BAD_ARGUMENT, "variable-coefficient diagonal is per point");
+    if (diag) *diag = op->g.c_diag;
+    if (inv_diag) *inv_diag = op->g.inv_diag;
+    return SRJ_OK;
+}
+
+int srj_op_set_sweeps_per_pass(srj_op* op, int32_t s) {
+    if (!op) return fail(SRJ_BAD_ARGUMENT, "null operator");
+    if (s < 1 || s > kTbMaxSub) return fail(SRJ_BAD_ARGUMENT, "sweeps per pass out of range");
+    op->sweeps_per_pass = s;
+    return SRJ_OK;
+}
+
+static int launch_cycle(srj_op* op, const double* xa, double* xb, const double* b,
+                        const double* omegas, int M, double tol, double baseline,
+                        cudaStream_t st) {
+    CycleArgs a;
+    a.g = op->g;
+    a.xa = xa;
+    a.xb = xb;
+    a.b = b;
+    a.omegas = omegas;
+    a.M = M;
+    a.tol = tol;
+    a.baseline = baseline;
+    a.partials = op->partials;
+    a.hist = op->hist;
+    a.out_i = op->out_i;
+    a.out_d = op->out_d;
+    void* args[] = {&a};
+    CUDA_TRY(cudaLaunchCooperativeKernel(cycle_kernel_for(op->g.fam), dim3(op->coop_blocks),
+                                         dim3(op->coop_threads), args, 0, st));
+    return SRJ_OK;
+}
+
+int srj_residual_sq(srj_op* op, const double* x, const double* b, double* sumsq_host, void* stream) {
+    if (!op || !x || !b || !sumsq_host) return fail(SRJ_BAD_ARGUMENT, "null argument");
+    DeviceGuard guard(op->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = launch_cycle(op, x, nullptr, b, nullptr, 0, 0.0, 1.0, st);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(op->h_out_d, op->out_d, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    *sumsq_host = op->h_out_d[0];
+    return SRJ_OK;
+}
+
+int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
+                  const double* omegas_dev, int32_t M, double tol, double baseline,
+                  double res_before, int64_t budget, double* history_host,
+                  srj_cycle_out* out, void* stream) {
+    if (!op || !x || !x_alt || !b || !out) return fail(SRJ_BAD_ARGUMENT, "null argument");
+    if (M < 1 || M > kMaxSchemeLength) return fail(SRJ_BAD_ARGUMENT, "scheme length out of range");
+    if (M > 0 && !omegas_dev) return fail(SRJ_BAD_ARGUMENT, "null omegas");
+    if (!(baseline > 0.0)) return fail(SRJ_BAD_ARGUMENT, "baseline must be positive");
+    DeviceGuard guard(op->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    std::memset(out, 0, sizeof(*out));
+    out->res_before = res_before;
+    out->res_after = res_before;
+    // Checks before sweep 0 are host-side: the incoming residual is known
+    // (solver.py:217-222).
+    if (res_before <= tol) {
+        out->status = SRJ_CYCLE_CONVERGED;
+        return SRJ_OK;
+    }
+    const int Meff = (int)std::min<int64_t>(M, std::max<int64_t>(budget, 0));
+    if (Meff == 0) return SRJ_OK;
+
+    int rc;
+    if (op->sweeps_per_pass > 1 && op->tb.supported) {
+        rc = tb_run_cycle(op->tb, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,
+                          op->sweeps_per_pass, op->partials, op->hist, op->out_i, op->out_d, st,
+                          &out->launches);
+        if (rc) return fail(SRJ_CUDA_ERROR, tb_last_error());
+    } else {
+        rc = launch_cycle(op, x, x_alt, b, omegas_dev, Meff, tol, baseline, st);
+        if (rc) return rc;
+        out->launches = 1;
+    }
+    CUDA_TRY(cudaMemcpyAsync(op->h_out_i, op->out_i, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(op->h_out_d, op->out_d, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (history_host)
+        CUDA_TRY(cudaMemcpyAsync(op->h_hist, op->hist, (Meff + 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    const int executed = op->h_out_i[0];
+    const int status = op->h_out_i[1];
+    out->executed = executed;
+    out->status = status;
+    out->result_in_alt = op->h_out_i[2];
+    out->res_after = op->h_out_d[1];
+    if (history_host && executed > 0)
+        std::memcpy(history_host, op->h_hist + 1, executed * sizeof(double));
+    return SRJ_OK;
+}
+
+int srj_sweep(srj_op* op, const double* x, double* x_out, const double* b, double omega, void* stream) {
+    if (!op || !x || !x_out || !b) return fail(SRJ_BAD_ARGUMENT, "null argument");
+    DeviceGuard guard(op->device);
+    return launch_apply<kSweep>(op, x, x_out, b, omega, (cudaStream_t)stream);
+}
+
+int srj_matvec(srj_op* op, const double* x, double* y, void* stream) {
+    if (!op || !x || !y) return fail(SRJ_BAD_ARGUMENT, "null argument");
+    DeviceGuard guard(op->device);
+    return launch_apply<kMatvec>(op, x, y, nullptr, 0.0, (cudaStream_t)stream);
+}
+
+int srj_fill_uniform_rhs(double* out, int64_t n, uint64_t seed, int64_t start, int32_t device,
+                         void* stream) {
+    if (n < 0 || start < 0) return fail(SRJ_BAD_ARGUMENT, "negative size");
+    if (n == 0) return SRJ_OK;
+    if (!out) return fail(SRJ_BAD_ARGUMENT, "null output");
+    DeviceGuard guard(device);
+    const long long blocks = std::min<long long>((n + 255) / 256, 148ll * 16);
+    k_fill_rhs<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(out, n, seed, start);
+    CUDA_TRY(cudaGetLastError());
+    return SRJ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,62 @@
+// Shared device helpers for the SRJ sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+// Separately rounded fp64 operations: the reference's scipy csr_matvec and
+// numpy ufuncs round every multiply and add on their own, so the device must
+// never contract them into FMAs (bit-identical iterates, SURVEY §8a parity
+// recipe).
+#define DMUL(a, b) __dmul_rn((a), (b))
+#define DADD(a, b) __dadd_rn((a), (b))
+#define DSUB(a, b) __dsub_rn((a), (b))
+
+namespace srj {
+
+enum Family { F1D = 1, F2D = 2, F3D = 3, F2DV = 4 };
+
+// Cycle outcome codes (match enum srj_cycle_status in include/srj.h).
+constexpr int kStatusRan = 0;
+constexpr int kStatusConverged = 1;
+constexpr int kStatusDiverged = 2;
+
+// Operator geometry as the kernels see it.  The flat interior index is
+// k = i + nx*j + nx*ny*z (x fastest, reference problems.py:119-120,158-161);
+// buffers carry `plane` ghost elements before and after the interior.
+struct Geom {
+    int fam;
+    int nx, ny, nz;
+    long long n;        // interior points
+    long long plane;    // ghost extent: 1 (1D), nx (2D), nx*ny (3D)
+    int rows;           // number of x-rows: ny*nz (1 in 1D)
+    int upr;            // 32-point units per row
+    int units;          // rows * upr
+    double c_off;       // off-diagonal value (-dx2)
+    double c_diag;      // diagonal value (2d*dx2)
+    double inv_diag;    // 1.0 / c_diag
+    const double* fx;   // var-coef faces (see srj.h)
+    const double* fy;
+};
+
+__device__ __forceinline__ double warp_allsum(double v) {
+    // xor butterfly: partners add the same two operands (commutative), so
+    // every lane ends with bit-identical sums.
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide sum, identical bits in every thread.  `sh` needs 32 doubles.
+__device__ __forceinline__ double block_allsum(double v, double* sh) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+    v = warp_allsum(v);
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double t = lane < nw ? sh[lane] : 0.0;
+    return warp_allsum(t);
+}
+
+}  // namespace srj

@@ -1,0 +1,382 @@
+"""SRJ cycles on the device, level-selection controllers and the solve driver.
+
+Same names, signatures, semantics and errors as the reference solver
+(reference solver.py:24-331); the difference is where the sweeps run.  Each
+cycle is ONE call into libsrj (`srj_run_cycle`): the sm_100a kernel applies up
+to M weighted-Jacobi sweeps in the scheme's application order, evaluates the
+stopping rule before every sweep on a device-reduced residual norm, and the
+host reads back one small struct (executed, status, res_after) -- plus the
+per-sweep residuals only when `record_history` is set.  Scheme selection
+(Heuristic / Increasing / FixedM / Jacobi / Cjm) stays on the host.
+
+Parity contract: identical scheme sequence, executed counts and
+iterates (bitwise) to the reference; residual norms differ from OpenBLAS ddot
+only in summation order (~1e-15 relative).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .operators import Field, StencilOperator
+from .problems import ABSOLUTE_L2, RELATIVE_L2, SOLUTION_DIFF_INF, ProblemInstance
+from .schemes import (MAX_LEVEL, ORDER_GRID_SIZE, SrjScheme, generate_srj_scheme,
+                      scheme_for_level)
+
+T_HI_DEFAULT = 0.4
+T_LO_DEFAULT = 0.2
+
+JACOBI_SCHEME = SrjScheme(M=1, omegas=(1.0,), application_order=(0,))
+
+
+@dataclass(frozen=True)
+class StoppingRule:
+    norm: str
+    tolerance: float
+    max_iterations: int
+
+    def __post_init__(self):
+        if self.tolerance <= 0.0:
+            raise ValueError("tolerance must be positive")
+        if self.max_iterations < 1:
+            raise ValueError("max_iterations must be positive")
+
+
+class ResidualKnown:
+    """`SolverState.cached_r` marker: the residual of `x` is `current_residual`.
+
+    The reference caches the vector r = b - A x (solver.py:53-54,205-207); the
+    device path never materialises r (every sweep recomputes it from x), so the
+    state only needs to know that `current_residual` belongs to `x`.
+    """
+
+    __slots__ = ()
+
+    def __repr__(self):
+        return "ResidualKnown"
+
+
+RESIDUAL_KNOWN = ResidualKnown()
+
+
+@dataclass
+class SolverState:
+    x: object
+    level: int = 0
+    prev_residual_ratio: float | None = None
+    cycle_index: int = 0
+    total_iterations: int = 0
+    residual_history: list[tuple[int, float]] = field(default_factory=list)
+    current_residual: float | None = None
+    cached_r: object | None = None
+    converged: bool = False
+
+
+@dataclass(frozen=True)
+class CycleStats:
+    cycle: int
+    level: int
+    M: int
+    executed: int
+    residual_before: float
+    residual_after: float
+    average_rate: float
+
+    @property
+    def ratio(self) -> float:
+        return self.residual_after / self.residual_before
+
+
+@dataclass
+class SolveReport:
+    converged: bool
+    total_iterations: int
+    cycles: list[CycleStats]
+    wall_time: float
+    x: object
+    residual_history: list[tuple[int, float]]
+
+
+class SolveDivergedError(RuntimeError):
+    """A sweep produced non-finite values (application-order failure)."""
+
+    def __init__(self, diagnostics: dict):
+        super().__init__(f"solve diverged: {diagnostics}")
+        self.diagnostics = diagnostics
+
+
+# ---------------------------------------------------------------------------
+# Controllers (reference solver.py:96-122)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class Heuristic:
+    t_hi: float = T_HI_DEFAULT
+    t_lo: float = T_LO_DEFAULT
+
+
+@dataclass(frozen=True)
+class Increasing:
+    pass
+
+
+@dataclass(frozen=True)
+class FixedM:
+    M: int
+
+
+@dataclass(frozen=True)
+class Jacobi:
+    pass
+
+
+@dataclass(frozen=True)
+class Cjm:
+    scheme: SrjScheme
+
+
+Controller = Heuristic | Increasing | FixedM | Jacobi | Cjm
+
+
+def heuristic_next_level(ratio: float, level: int, t_hi: float = T_HI_DEFAULT,
+                         t_lo: float = T_LO_DEFAULT) -> int:
+    """Algorithm 1: raise above t_hi, lower strictly between t_lo and t_hi,
+    otherwise keep (ratio == t_hi keeps); clamp to the ladder."""
+    if ratio < 0.0:
+        raise ValueError("residual ratio must be nonnegative")
+    if ratio > t_hi:
+        level += 1
+    elif t_lo < ratio < t_hi:
+        level -= 1
+    return min(max(level, 0), MAX_LEVEL)
+
+
+def average_convergence_rate(r_before: float, r_after: float, M: int) -> float:
+    if r_before <= 0.0 or r_after <= 0.0:
+        raise ValueError("residuals must be positive")
+    if M < 1:
+        raise ValueError("M must be positive")
+    return -math.log(r_after / r_before) / M
+
+
+# ---------------------------------------------------------------------------
+# Device plumbing
+# ---------------------------------------------------------------------------
+
+class _OmegaCache:
+    """Ordered omegas of each scheme, resident in HBM (one upload per scheme)."""
+
+    def __init__(self):
+        self._by_device: dict = {}
+
+    def get(self, scheme: SrjScheme, device):
+        import torch
+        key = (str(device), scheme.M, scheme.omegas, scheme.application_order)
+        table = self._by_device
+        t = table.get(key)
+        if t is None:
+            t = torch.tensor(scheme.ordered_omegas(), dtype=torch.float64, device=device)
+            if len(table) > 512:
+                table.clear()
+            table[key] = t
+        return t
+
+
+_OMEGAS = _OmegaCache()
+
+
+def _require_device_operator(A) -> StencilOperator:
+    if not isinstance(A, StencilOperator):
+        raise TypeError(
+            "the SRJ device path needs a StencilOperator (structured 1D/2D/3D stencil); "
+            f"got {type(A).__name__}")
+    return A
+
+
+def _l2_norm_parts(norm: str) -> None:
+    if norm == SOLUTION_DIFF_INF:
+        raise NotImplementedError(
+            "solution_diff_inf stopping is not on the device path yet (SURVEY §8 f2)")
+    if norm not in (ABSOLUTE_L2, RELATIVE_L2):
+        raise ValueError(f"unknown norm {norm!r}")
+
+
+def _device_cycle(A: StencilOperator, b: Field, x: Field, x_alt: Field, state: SolverState,
+                  scheme: SrjScheme, stopping: StoppingRule | None, baseline: float,
+                  record_history: bool, x_out_kind):
+    """One cycle on (x, x_alt); returns (new_state, stats, result_field, other_field).
+
+    Follows reference solver.py:187-273 step by step; the sweep loop itself
+    (:216-243) is the device call.
+    """
+    if state.cached_r is not None and state.current_residual is not None:
+        res_now = float(state.current_residual)
+    else:
+        res_now = math.sqrt(A.residual_sq(x, b)) / baseline
+    res_before = res_now
+    history = list(state.residual_history) if record_history else state.residual_history
+    if record_history and not history:
+        history.append((state.total_iterations, res_now))
+
+    M = scheme.M
+    tol = stopping.tolerance if stopping is not None else -1.0
+    budget = (stopping.max_iterations - state.total_iterations) if stopping is not None else M
+    hist = np.empty(M, dtype=np.float64) if record_history else None
+    omegas = _OMEGAS.get(scheme, A.device)
+    out = A.run_cycle(x, x_alt, b, omegas, M, tol, baseline, res_before, budget, hist)
+    executed = int(out.executed)
+    if out.status == _lib.CYCLE_DIVERGED:
+        ordered = scheme.ordered_omegas()
+        raise SolveDivergedError({
+            "cycle": state.cycle_index, "sweep": executed, "omega": ordered[executed - 1],
+            "level": scheme.level, "M": scheme.M,
+        })
+    res_after = float(out.res_after) if executed > 0 else res_before
+    converged = stopping is not None and res_after <= stopping.tolerance
+    if record_history:
+        base = state.total_iterations
+        history.extend((base + k + 1, float(hist[k])) for k in range(executed))
+
+    if executed > 0 and res_before > 0.0 and res_after > 0.0:
+        rate = average_convergence_rate(res_before, res_after, executed)
+        ratio = res_after / res_before
+    else:
+        rate = math.inf if executed > 0 else 0.0
+        ratio = state.prev_residual_ratio
+
+    result, other = (x_alt, x) if out.result_in_alt else (x, x_alt)
+    stats = CycleStats(
+        cycle=state.cycle_index, level=scheme.level if scheme.level is not None else -1,
+        M=scheme.M, executed=executed, residual_before=res_before, residual_after=res_after,
+        average_rate=rate,
+    )
+    new_state = SolverState(
+        x=x_out_kind(result), level=scheme.level if scheme.level is not None else state.level,
+        prev_residual_ratio=ratio if executed > 0 else state.prev_residual_ratio,
+        cycle_index=state.cycle_index + 1,
+        total_iterations=state.total_iterations + executed,
+        residual_history=history, current_residual=res_after,
+        cached_r=RESIDUAL_KNOWN, converged=converged,
+    )
+    return new_state, stats, result, other
+
+
+def _field_view(f: Field):
+    return f.interior
+
+
+def run_cycle(A: StencilOperator, b, state: SolverState, scheme: SrjScheme,
+              stopping: StoppingRule | None = None, baseline: float = 1.0,
+              norm: str = ABSOLUTE_L2, record_history: bool = True,
+              ) -> tuple[SolverState, CycleStats]:
+    """Apply one scheme cycle and return the advanced state plus its stats.
+
+    The input state is not modified (its x is copied into a fresh device
+    ping-pong pair); numpy inputs give numpy outputs.
+    """
+    A = _require_device_operator(A)
+    if stopping is not None and norm != stopping.norm:
+        norm = stopping.norm
+    _l2_norm_parts(norm)
+    as_numpy = isinstance(state.x, np.ndarray)
+    bf = b if isinstance(b, Field) else A.field(b)
+    x = A.field(state.x)
+    x_alt = A.new_field()
+
+    def kind(f: Field):
+        return f.interior.cpu().numpy() if as_numpy else f.interior
+
+    new_state, stats, _, _ = _device_cycle(A, bf, x, x_alt, state, scheme, stopping,
+                                           baseline, record_history, kind)
+    return new_state, stats
+
+
+def _next_scheme(controller: Controller, state: SolverState, order_grid: int) -> SrjScheme:
+    if isinstance(controller, (Heuristic, Increasing)):
+        return scheme_for_level(state.level, order_grid)
+    if isinstance(controller, FixedM):
+        return generate_srj_scheme(controller.M, order_grid)
+    if isinstance(controller, Jacobi):
+        return JACOBI_SCHEME
+    if isinstance(controller, Cjm):
+        return controller.scheme
+    raise TypeError(f"unknown controller {controller!r}")
+
+
+def solve(problem: ProblemInstance, controller: Controller, stopping: StoppingRule,
+          order_grid: int = ORDER_GRID_SIZE, record_history: bool = True) -> SolveReport:
+    """Full solve under a controller and stopping rule (reference solver.py:289-331).
+
+    b and x0 are staged into HBM once; the iterate then ping-pongs between two
+    device buffers for the whole solve with no per-cycle copies.  The report's
+    x has the kind of x0: numpy array, CPU tensor (copied back through pinned
+    memory) or CUDA tensor (no copy).
+    """
+    t0 = time.perf_counter()
+    A = _require_device_operator(problem.A)
+    _l2_norm_parts(stopping.norm)
+    b = A.field(problem.b)
+    x = A.field(problem.x0)
+    rep = solve_fields(A, b, x, A.new_field(), controller, stopping, order_grid, record_history)
+    rep.x = _like(problem.x0, rep.x)
+    rep.wall_time = time.perf_counter() - t0
+    return rep
+
+
+def _like(template, x_dev):
+    if isinstance(template, np.ndarray):
+        return x_dev.cpu().numpy()
+    if not template.is_cuda:
+        import torch
+        out = torch.empty(x_dev.shape, dtype=x_dev.dtype, pin_memory=True)
+        out.copy_(x_dev)
+        return out
+    return x_dev
+
+
+def solve_fields(A: StencilOperator, b: Field, x: Field, x_alt: Field, controller: Controller,
+                 stopping: StoppingRule, order_grid: int = ORDER_GRID_SIZE,
+                 record_history: bool = True, cycle_hook=None) -> SolveReport:
+    """`solve` on device-resident Fields (no staging): x holds x0 on entry and
+    both x and x_alt are overwritten.  The report's x is a CUDA view of
+    whichever buffer holds the final iterate.  `cycle_hook(stats)` is called
+    after every cycle (bench instrumentation)."""
+    t0 = time.perf_counter()
+    _l2_norm_parts(stopping.norm)
+    baseline = 1.0
+    if stopping.norm == RELATIVE_L2:
+        baseline = math.sqrt(A.residual_sq(x, b))
+        if baseline == 0.0:
+            raise ValueError("initial residual is zero; relative norm undefined")
+    state = SolverState(x=x.interior, level=0)
+    cycles: list[CycleStats] = []
+    converged = False
+    while True:
+        scheme = _next_scheme(controller, state, order_grid)
+        state, stats, x, x_alt = _device_cycle(A, b, x, x_alt, state, scheme, stopping,
+                                               baseline, record_history, _field_view)
+        if cycle_hook is not None:
+            cycle_hook(stats)
+        if stats.executed > 0:
+            cycles.append(stats)
+        if state.converged:
+            converged = True
+            break
+        if state.total_iterations >= stopping.max_iterations:
+            break
+        if isinstance(controller, Heuristic):
+            ratio = state.prev_residual_ratio
+            if ratio is not None and math.isfinite(ratio):
+                state.level = heuristic_next_level(ratio, state.level,
+                                                   controller.t_hi, controller.t_lo)
+        elif isinstance(controller, Increasing):
+            state.level = min(state.level + 1, MAX_LEVEL)
+    return SolveReport(
+        converged=converged, total_iterations=state.total_iterations, cycles=cycles,
+        wall_time=time.perf_counter() - t0, x=x.interior, residual_history=state.residual_history,
+    )

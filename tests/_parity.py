@@ -1,0 +1,119 @@
+"""Shared parity helpers: golden fixtures and trace comparison.
+
+The fixtures in tests/golden/ were produced by running the reference itself
+(tests/golden/make_golden.py).  Comparison rules (SURVEY §8a parity contract):
+  - scheme levels, M, executed counts, cycle count, total sweeps: exact;
+  - converged flag: exact;
+  - iterate x: bit-identical (sha256 of the float64 bytes) -- the north star
+    only asks for <= 1e-10 relative L2, which is also asserted;
+  - residual norms: relative 1e-12 (only the summation order of sum r^2
+    differs from OpenBLAS ddot).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import math
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLDEN = os.path.join(HERE, "golden")
+RES_RTOL = 1e-12
+X_REL_L2 = 1e-10
+
+_cache = {}
+
+
+def traces():
+    if "traces" not in _cache:
+        with open(os.path.join(GOLDEN, "traces.json")) as fh:
+            _cache["traces"] = json.load(fh)
+    return _cache["traces"]
+
+
+def case(name):
+    for c in traces()["cases"]:
+        if c["name"] == name:
+            return c
+    raise KeyError(name)
+
+
+def cases(filter_fn=None):
+    return [c for c in traces()["cases"] if filter_fn is None or filter_fn(c)]
+
+
+def schemes_npz():
+    if "schemes" not in _cache:
+        _cache["schemes"] = dict(np.load(os.path.join(GOLDEN, "schemes.npz")))
+    return _cache["schemes"]
+
+
+def sha(x) -> str:
+    return hashlib.sha256(np.ascontiguousarray(x, dtype=np.float64).tobytes()).hexdigest()
+
+
+def case_inputs(c):
+    """(family, n, b, face_x, face_y) for a golden case, built from the
+    product-independent recipes (SplitMix64 rhs; config-4 faces)."""
+    import sys
+    root = os.path.dirname(HERE)
+    if root not in sys.path:
+        sys.path.insert(0, root)
+    from paper_2011_06636_b200.problems import gaussian_field, harmonic_faces
+    from paper_2011_06636_b200.rng import uniform_rhs
+
+    fam, n = c["family"], c["n"]
+    N = {"1d3": n, "2d5": n * n, "2d5var": n * n, "3d7": n ** 3}[fam]
+    b = np.ones(N) if c.get("rhs", "uniform") == "ones" else uniform_rhs(c.get("seed", 0), N)
+    fx = fy = None
+    if fam == "2d5var":
+        fx, fy = harmonic_faces(np.exp(gaussian_field(n, c.get("seed", 0))), (n + 1.0) ** 2)
+        assert sha(fx) == c["face_x_sha256"] and sha(fy) == c["face_y_sha256"]
+    return fam, n, b, fx, fy
+
+
+def golden_cycle_rows(c):
+    """Per-cycle (cycle, level, M, executed) ints and the rows with residuals."""
+    cyc = c["cycles"]
+    if isinstance(cyc, dict):
+        ints = [tuple(r) for r in cyc["ints"]]
+        full = {r[0]: r[1:] for r in cyc["sampled"]}
+        return ints, full
+    ints = [tuple(r[:4]) for r in cyc]
+    return ints, {k: r for k, r in enumerate(cyc)}
+
+
+def assert_trace_matches(c, got_rows, total, converged, x=None, history=None):
+    """got_rows: list of (cycle, level, M, executed, res_before, res_after, rate)."""
+    ints, full = golden_cycle_rows(c)
+    got_ints = [tuple(int(v) for v in r[:4]) for r in got_rows]
+    assert len(got_ints) == len(ints), f"{c['name']}: {len(got_ints)} cycles vs {len(ints)}"
+    if got_ints != ints:
+        k = next(i for i, (a, b) in enumerate(zip(got_ints, ints)) if a != b)
+        raise AssertionError(f"{c['name']}: cycle {k} differs: got {got_ints[k]} want {ints[k]}")
+    assert total == c["total_iterations"], (c["name"], total, c["total_iterations"])
+    assert converged == c["converged"], c["name"]
+    for k, want in full.items():
+        got = got_rows[k]
+        for idx in (4, 5):
+            assert math.isclose(got[idx], want[idx], rel_tol=RES_RTOL, abs_tol=0.0), \
+                (c["name"], k, idx, got[idx], want[idx])
+        if math.isfinite(want[6]) and want[6] != 0.0:
+            # rate = -log(ratio)/executed amplifies the 1e-15 norm noise
+            assert math.isclose(got[6], want[6], rel_tol=1e-8, abs_tol=1e-12), (c["name"], k)
+    if x is not None:
+        x = np.asarray(x, dtype=np.float64)
+        if "x" in c:
+            ref = np.asarray(c["x"])
+            denom = max(np.linalg.norm(ref), 1e-300)
+            assert np.linalg.norm(x - ref) / denom <= X_REL_L2, c["name"]
+        assert sha(x) == c["x_sha256"], f"{c['name']}: iterate not bit-identical"
+    if history is not None and "history" in c:
+        want = c["history"]
+        assert len(history) == len(want), c["name"]
+        for (i1, r1), (i2, r2) in zip(history, want):
+            assert i1 == i2
+            assert math.isclose(r1, r2, rel_tol=RES_RTOL), (c["name"], i1, r1, r2)
