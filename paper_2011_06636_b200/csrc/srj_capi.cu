@@ -25,46 +25,17 @@
 #include "srj_common.cuh"
 #include "srj_stencil.cuh"
 #include "srj_tb.cuh"
+#include "srj_walk.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace srj {
 
 constexpr int kMaxSchemeLength = 10000;  // reference schemes.py:24
-constexpr int kThreads = 256;
+constexpr int kThreads = 256;       // standalone sweep / matvec kernels
+constexpr int kCoopThreads = 512;   // persistent cycle kernel: 2 CTAs per SM
 constexpr int kSmallThreads = 1024;
 constexpr long long kSmallUnits = 256;   // <= 8192 points: one CTA, no grid barrier
-
-enum Mode { kSweep = 0, kResid = 1, kMatvec = 2 };
-
-// Walk the 32-point x-row units [u0, u1): warps take units round-robin so a
-// CTA's warps stream through consecutive rows together (coalesced rows, and
-// the y/z neighbour rows are reused from L1/L2 while still hot).
-template <int FAM, int MODE>
-__device__ __forceinline__ double walk_units(const Geom& g, const double* x, double* out,
-                                             const double* __restrict__ b, double w,
-                                             int u0, int u1) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    double acc = 0.0;
-    for (int u = u0 + warp; u < u1; u += nw) {
-        const int row = u / g.upr;
-        const int i = (u - row * g.upr) * 32 + lane;
-        if (i < g.nx) {
-            const int j = (FAM == F3D) ? row % g.ny : row;
-            const long long k = (long long)row * g.nx + i;
-            double xc, inv;
-            const double y = apply_at<FAM>(g, x, k, i, j, xc, inv);
-            if constexpr (MODE == kMatvec) {
-                out[k] = y;
-            } else {
-                const double r = DSUB(__ldg(b + k), y);
-                acc = fma(r, r, acc);
-                if constexpr (MODE == kSweep) out[k] = relax(xc, inv, r, w);
-            }
-        }
-    }
-    return acc;
-}
 
 struct CycleArgs {
     Geom g;
@@ -79,14 +50,6 @@ struct CycleArgs {
     int* out_i;            // executed, status
     double* out_d;         // final sum of squares, res_after
 };
-
-__device__ __forceinline__ void grid_barrier() {
-    if (gridDim.x == 1) {
-        __syncthreads();
-    } else {
-        cg::this_grid().sync();
-    }
-}
 
 template <int FAM>
 __global__ void __launch_bounds__(1024) k_cycle(CycleArgs a) {
@@ -107,9 +70,7 @@ __global__ void __launch_bounds__(1024) k_cycle(CycleArgs a) {
         if (threadIdx.x == 0) part[blockIdx.x] = acc;
         grid_barrier();
         if (k >= 1 || tail) {
-            double s = 0.0;
-            for (int q = threadIdx.x; q < nb; q += blockDim.x) s += __ldcg(part + q);
-            S = block_allsum(s, sh);
+            S = reduce_partials(part, nb, sh);
             res = sqrt(S) / a.baseline;
             if (k >= 1) {
                 if (blockIdx.x == 0 && threadIdx.x == 0) a.hist[k] = res;
@@ -288,13 +249,14 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
         op->coop_threads = kSmallThreads;
     } else {
         int per_sm = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cycle_kernel_for(g.fam), kThreads, 0);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cycle_kernel_for(g.fam), kCoopThreads, 0);
         if (e != cudaSuccess || per_sm < 1) { delete op; return fail(SRJ_CUDA_ERROR, "occupancy query failed"); }
-        long long want = (long long)per_sm * op->num_sms;
-        // at least ~4 units per warp keeps the per-sweep reduction cheap
-        const long long cap = std::max<long long>(1, g.units / (4 * (kThreads / 32)));
+        // Few, fat CTAs: the per-sweep grid barrier and partial reduction cost
+        // grows with the CTA count.
+        long long want = (long long)std::min(per_sm, 2) * op->num_sms;
+        const long long cap = std::max<long long>(1, g.units / (4 * (kCoopThreads / 32)));
         op->coop_blocks = (int)std::min(want, cap);
-        op->coop_threads = kThreads;
+        op->coop_threads = kCoopThreads;
     }
     const size_t nparts = 2 * (size_t)std::max(op->coop_blocks, 8 * op->num_sms) * kTbMaxSub;
     if ((e = cudaMalloc(&op->partials, nparts * sizeof(double))) != cudaSuccess ||
@@ -307,7 +269,10 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("allocation failed: ") + cudaGetErrorString(e));
     }
-    tb_plan_init(op->tb, g, op->num_sms);
+    if ((e = tb_plan_init(op->tb, g, op->num_sms)) != cudaSuccess) {
+        srj_op_destroy(op);
+        return fail(SRJ_CUDA_ERROR, std::string("temporal-blocking setup failed: ") + cudaGetErrorString(e));
+    }
     *out = op;
     return SRJ_OK;
 }
@@ -404,14 +369,13 @@ int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
     const int Meff = (int)std::min<int64_t>(M, std::max<int64_t>(budget, 0));
     if (Meff == 0) return SRJ_OK;
 
-    int rc;
     if (op->sweeps_per_pass > 1 && op->tb.supported) {
-        rc = tb_run_cycle(op->tb, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,
-                          op->sweeps_per_pass, op->partials, op->hist, op->out_i, op->out_d, st,
-                          &out->launches);
-        if (rc) return fail(SRJ_CUDA_ERROR, tb_last_error());
+        CUDA_TRY(tb_launch_cycle(op->tb, op->g, x, x_alt, b, omegas_dev, Meff,
+                                 op->sweeps_per_pass, tol, baseline, op->partials, op->hist,
+                                 op->out_i, op->out_d, st));
+        out->launches = 1;
     } else {
-        rc = launch_cycle(op, x, x_alt, b, omegas_dev, Meff, tol, baseline, st);
+        const int rc = launch_cycle(op, x, x_alt, b, omegas_dev, Meff, tol, baseline, st);
         if (rc) return rc;
         out->launches = 1;
     }

@@ -1,26 +1,34 @@
-// Temporal blocking: several SRJ sweeps per HBM pass (declarations).
+// Temporal blocking: several SRJ sweeps per HBM/L2 pass (declarations).
 #pragma once
 
 #include <cuda_runtime.h>
+#include <stddef.h>
 
 #include "srj_common.cuh"
 
 namespace srj {
 
-constexpr int kTbMaxSub = 16;  // most sweeps fused into one pass
+constexpr int kTbMaxSub = 8;  // most sweeps fused into one pass
 
 struct TbPlan {
     bool supported = false;
-    int num_sms = 0;
+    int blocks = 0;      // cooperative grid (one CTA per SM)
+    int threads = 0;
+    size_t smem = 0;     // dynamic shared memory per CTA
+    int tiles_x = 0;
+    int ntiles = 0;
 };
 
-void tb_plan_init(TbPlan& plan, const Geom& g, int num_sms);
+// Decide whether the operator has a temporal-blocking kernel and size its grid.
+cudaError_t tb_plan_init(TbPlan& plan, const Geom& g, int num_sms);
 
-int tb_run_cycle(TbPlan& plan, const Geom& g, double* x, double* x_alt, const double* b,
-                 const double* omegas, int M, double tol, double baseline, int s,
-                 double* partials, double* hist, int* out_i, double* out_d, cudaStream_t st,
-                 int* launches);
-
-const char* tb_last_error();
+// Launch one cycle of M sweeps, s per pass (1 <= s <= kTbMaxSub).  Same
+// outputs as the one-sweep cycle kernel: out_i = {executed, status, result
+// buffer (0: x, 1: x_alt)}, out_d = {final sum of squares, res_after};
+// hist[k] = relative residual of x_k for k = 1..executed.
+cudaError_t tb_launch_cycle(const TbPlan& plan, const Geom& g, double* x, double* x_alt,
+                            const double* b, const double* omegas, int M, int s, double tol,
+                            double baseline, double* partials, double* hist, int* out_i,
+                            double* out_d, cudaStream_t st);
 
 }  // namespace srj

@@ -112,3 +112,19 @@ def test_solve_is_deterministic_on_device():
     assert a.total_iterations == b.total_iterations
     assert np.array_equal(a.x, b.x)
     assert [r.residual_after for r in a.cycles] == [r.residual_after for r in b.cycles]
+
+
+# --------------------------------------------------------------------------
+# Temporal blocking (several sweeps per pass, rollback on a mid-pass stop)
+# --------------------------------------------------------------------------
+
+TB_NAMES = [c["name"] for c in P.cases(lambda c: c["family"] == "2d5" and "diverged" not in c)]
+
+
+@pytest.mark.parametrize("spp", [2, 3, 8])
+@pytest.mark.parametrize("name", TB_NAMES)
+def test_temporal_blocking_matches_reference(name, spp):
+    c = P.case(name)
+    rep = device_solve(c, record_history="history" in c, sweeps_per_pass=spp)
+    P.assert_trace_matches(c, rows_of(rep), rep.total_iterations, rep.converged, x=rep.x,
+                           history=rep.residual_history if "history" in c else None)
