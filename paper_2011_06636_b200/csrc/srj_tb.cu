@@ -1,39 +1,58 @@
 // Temporally blocked SRJ cycle for the 2D 5-point constant-coefficient
-// stencil (BASELINE config 2): s consecutive sweeps, each with its own omega,
-// per HBM/L2 round trip.
+// stencil (BASELINE config 2): up to S consecutive sweeps, each with its own
+// omega, per HBM/L2 round trip of x and b.
 //
-// Overlapped ("ghost-zone") tiling: a CTA owns a TX x TY output tile and loads
-// the (TX+2S) x (TY+2S) region around it into shared memory once per pass.
-// Sub-sweep t (0..h-1) updates the region shrunk by t+1 rings, ping-ponging
-// between two shared buffers, so after h sub-sweeps the owned tile holds
-// x_{k0+h} exactly -- every value is produced by the same per-point arithmetic
-// as the one-sweep kernel (bit-identical iterates).  Points outside the grid
-// stay 0 in both buffers, which is the Dirichlet ghost.
+// Tiling.  A CTA (one per SM, persistent, cooperative launch) owns 64 x 64
+// output tiles.  For each tile the copy engine (TMA) brings the (64+2S)^2 region
+// of x_{k0} and b into shared memory; boxes that stick out of the grid are
+// zero-filled, which is the Dirichlet ghost.  The next tile's boxes are
+// prefetched while the current tile computes.
 //
-// Residuals: sub-sweep t accumulates (b - A x_{k0+t})^2 over OWNED points only,
-// giving per-sweep partials identical in meaning to the one-sweep kernel.  After
-// each pass a grid barrier lets every CTA reduce the s partial vectors in a fixed
-// order and apply the reference's per-sweep stopping rule (solver.py:216-222,
-// 235-239).  A stop inside the pass at sweep k0+j (j >= 1) is resolved by
-// re-running that pass with j sub-sweeps from its intact input buffer
-// (rollback); a stop at j = 0 returns the input buffer itself.
+// Register tiling.  Thread (c, seg) keeps rows [seg*V, seg*V+V) of region
+// column c in registers; per sub-sweep it publishes them to a shared exchange
+// buffer and reads only its west/east neighbours (plus one row above and below
+// its segment) back: ~3 shared accesses per point instead of 6, and V
+// independent fp64 dependency chains per thread.  Every point of the region is
+// updated every sub-sweep (no divergence); values within t+1 rings of the
+// region edge are garbage after sub-sweep t but never reach the owned tile,
+// which after h <= S sub-sweeps holds x_{k0+h} exactly -- each value produced
+// by the per-point arithmetic of the one-sweep kernel (bit-identical iterates).
+// Grid-exterior points are held at 0.
+//
+// Residuals.  Sub-sweep t accumulates (b - A x_{k0+t})^2 over OWNED points only,
+// so the per-CTA partials have the meaning of the one-sweep kernel's.  After a
+// pass a grid barrier lets every CTA reduce them in a fixed order and apply the
+// reference's per-sweep stopping rule (solver.py:216-222,235-239).  A stop at
+// sweep k0+j, j >= 1, re-runs the pass with j sub-sweeps from its intact input
+// buffer (rollback); j = 0 returns the input buffer itself.
 #include <cooperative_groups.h>
 
 #include <algorithm>
 
 #include "srj_stencil.cuh"
 #include "srj_tb.cuh"
+#include "srj_tma.cuh"
 #include "srj_walk.cuh"
 
 namespace srj {
 namespace tb2d {
-constexpr int TX = 64, TY = 64, SMAX = kTbMaxSub;
-constexpr int RX = TX + 2 * SMAX, RY = TY + 2 * SMAX;  // 80 x 80 region
-constexpr int THREADS = 640;
-constexpr int G = THREADS / RX;          // row groups
-constexpr int ROWS = (RY + G - 1) / G;   // region rows per thread
-static_assert(THREADS % RX == 0, "thread rows must tile the region width");
-constexpr size_t SMEM = 2ull * RX * RY * sizeof(double);
+
+template <int S>
+struct Cfg {
+    static constexpr int TX = 64, TY = 64;
+    static constexpr int RX = TX + 2 * S, RY = TY + 2 * S;
+    static constexpr int NSEG = 8;
+    static constexpr int V = RY / NSEG;
+    static_assert(RY % NSEG == 0, "segments must tile the region height");
+    static constexpr int THREADS = RX * NSEG;
+    static constexpr int EP = RX + 2;        // exchange buffer pitch (zero border)
+    static constexpr int EROWS = RY + 2;
+    static constexpr int STAGE = RX * RY;    // doubles per staged box
+    static constexpr int EX = EP * EROWS;    // doubles per exchange buffer
+    static constexpr size_t SMEM = (size_t)(2 * STAGE + 2 * EX) * sizeof(double) + 16;
+    static constexpr uint32_t TX_BYTES = 2u * STAGE * sizeof(double);
+};
+
 }  // namespace tb2d
 
 struct TbArgs {
@@ -44,112 +63,150 @@ struct TbArgs {
     const double* omegas;
     int M, s;
     double tol, baseline;
-    double* partials;  // [2][SMAX][gridDim.x]
+    double* partials;  // [2][kTbMaxSub][gridDim.x]
     double* hist;
     int* out_i;
     double* out_d;
     int tiles_x, ntiles;
 };
 
-// One pass (h sub-sweeps) over every tile this CTA owns.
-__device__ __forceinline__ void tb2d_pass(const TbArgs& a, const double* __restrict__ xin,
-                                          double* __restrict__ xout, int k0, int h,
-                                          double (&acc)[tb2d::SMAX], bool accumulate,
-                                          double* xs0, double* xs1) {
-    using namespace tb2d;
+template <int S>
+struct TbSmem {
+    double* stx;
+    double* stb;
+    double* E0;
+    double* E1;
+    uint64_t* bar;
+};
+
+template <int S>
+__device__ __forceinline__ void tb2d_issue(const TbArgs& a, const CUtensorMap* tm_in,
+                                           const CUtensorMap* tm_b, const TbSmem<S>& sm, int q) {
+    using C = tb2d::Cfg<S>;
+    const int ox = (q % a.tiles_x) * C::TX, oy = (q / a.tiles_x) * C::TY;
+    fence_proxy_async();
+    mbar_expect_tx(sm.bar, C::TX_BYTES);
+    tma_load_2d(sm.stx, tm_in, ox - S, oy - S, sm.bar);
+    tma_load_2d(sm.stb, tm_b, ox - S, oy - S, sm.bar);
+}
+
+// One pass (h sub-sweeps, h <= S) over every tile this CTA owns.
+template <int S>
+__device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm_in,
+                                          const CUtensorMap* tm_b, double* __restrict__ xout,
+                                          int k0, int h, double (&acc)[S], bool accumulate,
+                                          const TbSmem<S>& sm, uint32_t& phase) {
+    using C = tb2d::Cfg<S>;
+    constexpr int V = C::V, RX = C::RX, EP = C::EP;
     const int tid = threadIdx.x;
-    const int c = tid % RX, gq = tid / RX;
+    const int c = tid % RX, seg = tid / RX, r0 = seg * V;
     const int nx = a.g.nx, ny = a.g.ny;
     const double coff = a.g.c_off, cdiag = a.g.c_diag, inv = a.g.inv_diag;
+    if ((int)blockIdx.x >= a.ntiles) return;
+    if (tid == 0) tb2d_issue<S>(a, tm_in, tm_b, sm, blockIdx.x);
     for (int q = blockIdx.x; q < a.ntiles; q += gridDim.x) {
-        const int ox = (q % a.tiles_x) * TX, oy = (q / a.tiles_x) * TY;
-        const int gx = ox - SMAX + c;
+        const int ox = (q % a.tiles_x) * C::TX, oy = (q / a.tiles_x) * C::TY;
+        const int gx = ox - S + c;
+        const int gy0 = oy - S + r0;
         const bool colin = gx >= 0 && gx < nx;
-        double breg[ROWS];
+        const bool ocol = c >= S && c < S + C::TX;
+        mbar_wait(sm.bar, phase);
+        phase ^= 1u;
+        double xr[V], br[V];
 #pragma unroll
-        for (int m = 0; m < ROWS; ++m) {
-            const int r = gq + G * m;
-            breg[m] = 0.0;
-            if (r < RY) {
-                const int gy = oy - SMAX + r;
-                const bool in = colin && gy >= 0 && gy < ny;
-                const long long k = (long long)gy * nx + gx;
-                xs0[r * RX + c] = in ? xin[k] : 0.0;
-                xs1[r * RX + c] = 0.0;
-                if (in) breg[m] = __ldg(a.b + k);
-            }
+        for (int v = 0; v < V; ++v) {
+            xr[v] = sm.stx[(r0 + v) * RX + c];
+            br[v] = sm.stb[(r0 + v) * RX + c];
+            sm.E0[(r0 + v + 1) * EP + c + 1] = xr[v];
         }
-        __syncthreads();
+        __syncthreads();  // staging consumed, E0 published
+        if (tid == 0 && q + (int)gridDim.x < a.ntiles)
+            tb2d_issue<S>(a, tm_in, tm_b, sm, q + gridDim.x);
 #pragma unroll
-        for (int t = 0; t < SMAX; ++t) {
+        for (int t = 0; t < S; ++t) {
             if (t < h) {
                 const double w = __ldg(a.omegas + k0 + t);
-                const double* src = (t & 1) ? xs1 : xs0;
-                double* dst = (t & 1) ? xs0 : xs1;
-                const int lo = SMAX - h + t + 1;
-                const int hix = SMAX + TX + h - t - 1, hiy = SMAX + TY + h - t - 1;
-                if (c >= lo && c < hix && colin) {
-                    const bool ocol = c >= SMAX && c < SMAX + TX;
+                const double* Ein = (t & 1) ? sm.E1 : sm.E0;
+                double* Eout = (t & 1) ? sm.E0 : sm.E1;
+                const double hs = Ein[r0 * EP + c + 1];
+                const double hn = Ein[(r0 + V + 1) * EP + c + 1];
+                double nr[V];
 #pragma unroll
-                    for (int m = 0; m < ROWS; ++m) {
-                        const int r = gq + G * m;
-                        const int gy = oy - SMAX + r;
-                        if (r >= lo && r < hiy && gy >= 0 && gy < ny) {
-                            const double* s0 = src + r * RX + c;
-                            const double xc = s0[0];
-                            double y = DADD(0.0, DMUL(coff, s0[-RX]));
-                            y = DADD(y, DMUL(coff, s0[-1]));
-                            y = DADD(y, DMUL(cdiag, xc));
-                            y = DADD(y, DMUL(coff, s0[1]));
-                            y = DADD(y, DMUL(coff, s0[RX]));
-                            const double rr = DSUB(breg[m], y);
-                            dst[r * RX + c] = relax(xc, inv, rr, w);
-                            if (accumulate && ocol && r >= SMAX && r < SMAX + TY)
-                                acc[t] = fma(rr, rr, acc[t]);
-                        }
-                    }
+                for (int v = 0; v < V; ++v) {
+                    const double* e = Ein + (r0 + v + 1) * EP + c;
+                    const double xs = v == 0 ? hs : xr[v - 1];
+                    const double xn = v == V - 1 ? hn : xr[v + 1];
+                    double y = DADD(0.0, DMUL(coff, xs));
+                    y = DADD(y, DMUL(coff, e[0]));
+                    y = DADD(y, DMUL(cdiag, xr[v]));
+                    y = DADD(y, DMUL(coff, e[2]));
+                    y = DADD(y, DMUL(coff, xn));
+                    const double rr = DSUB(br[v], y);
+                    const int gy = gy0 + v;
+                    const bool in = colin && gy >= 0 && gy < ny;
+                    nr[v] = in ? relax(xr[v], inv, rr, w) : 0.0;
+                    const int r = r0 + v;
+                    if (accumulate && in && ocol && r >= S && r < S + C::TY)
+                        acc[t] = fma(rr, rr, acc[t]);
+                }
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    Eout[(r0 + v + 1) * EP + c + 1] = nr[v];
+                    xr[v] = nr[v];
                 }
                 __syncthreads();
             }
         }
-        const double* fin = (h & 1) ? xs1 : xs0;
-        if (c >= SMAX && c < SMAX + TX && colin) {
+        if (ocol && colin) {
 #pragma unroll
-            for (int m = 0; m < ROWS; ++m) {
-                const int r = gq + G * m;
-                const int gy = oy - SMAX + r;
-                if (r >= SMAX && r < SMAX + TY && gy < ny)
-                    xout[(long long)gy * nx + gx] = fin[r * RX + c];
+            for (int v = 0; v < V; ++v) {
+                const int r = r0 + v, gy = gy0 + v;
+                if (r >= S && r < S + C::TY && gy < ny) xout[(long long)gy * nx + gx] = xr[v];
             }
         }
-        __syncthreads();
     }
 }
 
-__global__ void __launch_bounds__(tb2d::THREADS, 1) k_tb2d_cycle(TbArgs a) {
-    using namespace tb2d;
-    extern __shared__ double smem[];
+template <int S>
+__global__ void __launch_bounds__(tb2d::Cfg<S>::THREADS, 1)
+    k_tb2d_cycle(const __grid_constant__ CUtensorMap tm_x0,
+                 const __grid_constant__ CUtensorMap tm_x1,
+                 const __grid_constant__ CUtensorMap tm_b, TbArgs a) {
+    using C = tb2d::Cfg<S>;
+    extern __shared__ __align__(128) double smem[];
     __shared__ double sh[32];
-    double* xs0 = smem;
-    double* xs1 = smem + RX * RY;
+    TbSmem<S> sm;
+    sm.stx = smem;
+    sm.stb = smem + C::STAGE;
+    sm.E0 = smem + 2 * C::STAGE;
+    sm.E1 = sm.E0 + C::EX;
+    sm.bar = reinterpret_cast<uint64_t*>(sm.E1 + C::EX);
+    for (int i = threadIdx.x; i < 2 * C::EX; i += blockDim.x) sm.E0[i] = 0.0;
+    if (threadIdx.x == 0) {
+        mbar_init(sm.bar, 1);
+        prefetch_tensormap(&tm_x0);
+        prefetch_tensormap(&tm_x1);
+        prefetch_tensormap(&tm_b);
+    }
+    __syncthreads();
+    uint32_t phase = 0;
     const int nb = gridDim.x;
     double* const buf[2] = {a.buf0, a.buf1};
+    const CUtensorMap* const tmx[2] = {&tm_x0, &tm_x1};
     const int npasses = (a.M + a.s - 1) / a.s;
     int executed = a.M, status = kStatusRan, result = npasses & 1;
-    double S = 0.0, res = 0.0;
+    double S2 = 0.0, res = 0.0;
     bool stopped = false;
     for (int p = 0; p < npasses && !stopped; ++p) {
         const int k0 = p * a.s;
         const int h = min(a.s, a.M - k0);
-        const double* xin = buf[p & 1];
-        double* xout = buf[(p + 1) & 1];
-        double acc[SMAX];
+        double acc[S];
 #pragma unroll
-        for (int t = 0; t < SMAX; ++t) acc[t] = 0.0;
-        tb2d_pass(a, xin, xout, k0, h, acc, true, xs0, xs1);
-        double* part = a.partials + (size_t)(p & 1) * SMAX * nb;
+        for (int t = 0; t < S; ++t) acc[t] = 0.0;
+        tb2d_pass<S>(a, tmx[p & 1], &tm_b, buf[(p + 1) & 1], k0, h, acc, true, sm, phase);
+        double* part = a.partials + (size_t)(p & 1) * kTbMaxSub * nb;
 #pragma unroll
-        for (int t = 0; t < SMAX; ++t) {
+        for (int t = 0; t < S; ++t) {
             if (t < h) {
                 const double v = block_allsum(acc[t], sh);
                 if (threadIdx.x == 0) part[t * nb + blockIdx.x] = v;
@@ -160,8 +217,8 @@ __global__ void __launch_bounds__(tb2d::THREADS, 1) k_tb2d_cycle(TbArgs a) {
         for (int t = 0; t < h; ++t) {
             const int k = k0 + t;
             if (k == 0) continue;  // res(x_0) is known to the host
-            S = reduce_partials(part + t * nb, nb, sh);
-            res = sqrt(S) / a.baseline;
+            S2 = reduce_partials(part + t * nb, nb, sh);
+            res = sqrt(S2) / a.baseline;
             if (blockIdx.x == 0 && threadIdx.x == 0) a.hist[k] = res;
             if (!isfinite(res)) { status = kStatusDiverged; stop_t = t; break; }
             if (res <= a.tol) { status = kStatusConverged; stop_t = t; break; }
@@ -173,7 +230,8 @@ __global__ void __launch_bounds__(tb2d::THREADS, 1) k_tb2d_cycle(TbArgs a) {
                 result = p & 1;
             } else {
                 // rollback: x_{k0+stop_t} from the intact pass input
-                tb2d_pass(a, xin, xout, k0, stop_t, acc, false, xs0, xs1);
+                tb2d_pass<S>(a, tmx[p & 1], &tm_b, buf[(p + 1) & 1], k0, stop_t, acc, false, sm,
+                             phase);
                 grid_barrier();
                 result = (p + 1) & 1;
             }
@@ -184,12 +242,12 @@ __global__ void __launch_bounds__(tb2d::THREADS, 1) k_tb2d_cycle(TbArgs a) {
         const int u0 = (int)((long long)a.g.units * blockIdx.x / nb);
         const int u1 = (int)((long long)a.g.units * (blockIdx.x + 1) / nb);
         double acc = walk_units<F2D, kResid>(a.g, buf[result], nullptr, a.b, 0.0, u0, u1);
-        double* part = a.partials + (size_t)(npasses & 1) * SMAX * nb;
+        double* part = a.partials + (size_t)(npasses & 1) * kTbMaxSub * nb;
         acc = block_allsum(acc, sh);
         if (threadIdx.x == 0) part[blockIdx.x] = acc;
         grid_barrier();
-        S = reduce_partials(part, nb, sh);
-        res = sqrt(S) / a.baseline;
+        S2 = reduce_partials(part, nb, sh);
+        res = sqrt(S2) / a.baseline;
         if (blockIdx.x == 0 && threadIdx.x == 0) a.hist[a.M] = res;
         if (!isfinite(res)) status = kStatusDiverged;
         else if (res <= a.tol) status = kStatusConverged;
@@ -198,35 +256,89 @@ __global__ void __launch_bounds__(tb2d::THREADS, 1) k_tb2d_cycle(TbArgs a) {
         a.out_i[0] = executed;
         a.out_i[1] = status;
         a.out_i[2] = result;
-        a.out_d[0] = S;
+        a.out_d[0] = S2;
         a.out_d[1] = res;
     }
 }
 
+// ----------------------------------------------------------------------------
+// Host side
+// ----------------------------------------------------------------------------
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+    }
+    return fn;
+}
+
+cudaError_t encode_field_map(CUtensorMap* map, const double* base, int nx, int ny, int box_x,
+                             int box_y) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return cudaErrorNotSupported;
+    const cuuint64_t dims[2] = {(cuuint64_t)nx, (cuuint64_t)ny};
+    const cuuint64_t strides[1] = {(cuuint64_t)nx * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)box_x, (cuuint32_t)box_y};
+    const cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
+                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int S>
+static cudaError_t setup_variant(int& per_sm) {
+    using C = tb2d::Cfg<S>;
+    cudaError_t e = cudaFuncSetAttribute(k_tb2d_cycle<S>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tb2d_cycle<S>, C::THREADS,
+                                                         C::SMEM);
+}
+
 cudaError_t tb_plan_init(TbPlan& plan, const Geom& g, int num_sms) {
     plan = TbPlan();
-    if (g.fam != F2D) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(k_tb2d_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)tb2d::SMEM);
+    // TMA needs 16-byte row pitch: even nx.
+    if (g.fam != F2D || (g.nx & 1) || !encode_fn()) return cudaSuccess;
+    int per4 = 0, per8 = 0;
+    cudaError_t e = setup_variant<4>(per4);
     if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tb2d_cycle, tb2d::THREADS,
-                                                      tb2d::SMEM);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) return cudaSuccess;
-    plan.tiles_x = (g.nx + tb2d::TX - 1) / tb2d::TX;
-    plan.ntiles = plan.tiles_x * ((g.ny + tb2d::TY - 1) / tb2d::TY);
-    plan.blocks = std::max(1, std::min(num_sms * per_sm, plan.ntiles));
-    plan.threads = tb2d::THREADS;
-    plan.smem = tb2d::SMEM;
+    if ((e = setup_variant<8>(per8)) != cudaSuccess) return e;
+    if (per4 < 1 || per8 < 1) return cudaSuccess;
+    plan.tiles_x = (g.nx + 63) / 64;
+    plan.ntiles = plan.tiles_x * ((g.ny + 63) / 64);
+    plan.blocks = std::max(1, std::min(num_sms, plan.ntiles));
     plan.supported = true;
     return cudaSuccess;
+}
+
+template <int S>
+static cudaError_t launch_variant(const TbPlan& plan, const CUtensorMap (&maps)[3], TbArgs& a,
+                                  cudaStream_t st) {
+    using C = tb2d::Cfg<S>;
+    CUtensorMap m0 = maps[0], m1 = maps[1], mb = maps[2];
+    void* args[] = {&m0, &m1, &mb, &a};
+    return cudaLaunchCooperativeKernel((const void*)k_tb2d_cycle<S>, dim3(plan.blocks),
+                                       dim3(C::THREADS), args, C::SMEM, st);
 }
 
 cudaError_t tb_launch_cycle(const TbPlan& plan, const Geom& g, double* x, double* x_alt,
                             const double* b, const double* omegas, int M, int s, double tol,
                             double baseline, double* partials, double* hist, int* out_i,
                             double* out_d, cudaStream_t st) {
+    if ((((uintptr_t)x | (uintptr_t)x_alt | (uintptr_t)b) & 15) != 0)
+        return cudaErrorMisalignedAddress;
     TbArgs a;
     a.g = g;
     a.buf0 = x;
@@ -243,9 +355,14 @@ cudaError_t tb_launch_cycle(const TbPlan& plan, const Geom& g, double* x, double
     a.out_d = out_d;
     a.tiles_x = plan.tiles_x;
     a.ntiles = plan.ntiles;
-    void* args[] = {&a};
-    return cudaLaunchCooperativeKernel((const void*)k_tb2d_cycle, dim3(plan.blocks),
-                                       dim3(plan.threads), args, plan.smem, st);
+    const int S = a.s <= 4 ? 4 : 8;
+    const int box = 64 + 2 * S;
+    CUtensorMap maps[3];
+    cudaError_t e;
+    if ((e = encode_field_map(&maps[0], x, g.nx, g.ny, box, box)) != cudaSuccess) return e;
+    if ((e = encode_field_map(&maps[1], x_alt, g.nx, g.ny, box, box)) != cudaSuccess) return e;
+    if ((e = encode_field_map(&maps[2], b, g.nx, g.ny, box, box)) != cudaSuccess) return e;
+    return S == 4 ? launch_variant<4>(plan, maps, a, st) : launch_variant<8>(plan, maps, a, st);
 }
 
 }  // namespace srj

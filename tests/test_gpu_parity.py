@@ -121,7 +121,7 @@ def test_solve_is_deterministic_on_device():
 TB_NAMES = [c["name"] for c in P.cases(lambda c: c["family"] == "2d5" and "diverged" not in c)]
 
 
-@pytest.mark.parametrize("spp", [2, 3, 8])
+@pytest.mark.parametrize("spp", [1, 2, 3, 5, 8])
 @pytest.mark.parametrize("name", TB_NAMES)
 def test_temporal_blocking_matches_reference(name, spp):
     c = P.case(name)
