@@ -108,8 +108,23 @@ int srj_op_layout(const srj_op* op, int64_t* n, int64_t* halo);
 /* Diagonal value and its reciprocal for constant-coefficient families
  * (diag = 2d*dx2, inv = 1/diag as the reference's SparseMatrix caches it). */
 int srj_op_diag(const srj_op* op, double* diag, double* inv_diag);
-/* Temporal blocking: sweeps fused per HBM pass (1 = one sweep per pass). */
+/* Temporal blocking: sweeps fused per HBM pass (1 = one sweep per pass).
+ * Values > 1 take effect only where a temporally blocked kernel exists for the
+ * operator (srj_op_info.tb_supported); elsewhere cycles run one sweep per pass. */
 int srj_op_set_sweeps_per_pass(srj_op* op, int32_t s);
+
+/* Launch configuration the handle chose (diagnostics and tests). */
+typedef struct srj_op_info {
+    int32_t num_sms;
+    int32_t cycle_blocks;      /* one-sweep cycle kernel: cooperative grid */
+    int32_t cycle_threads;
+    int32_t sweeps_per_pass;   /* current setting */
+    int32_t tb_supported;      /* 1 if a temporally blocked kernel serves this operator */
+    int32_t tb_blocks;
+    int32_t tb_occupancy;      /* resident CTAs per SM of the smallest TB variant */
+    int32_t tb_tiles;
+} srj_op_info;
+int srj_op_describe(const srj_op* op, srj_op_info* info);
 
 /* sum_i (b - A x)_i^2 -> *sumsq_host.  Synchronises `stream`. */
 int srj_residual_sq(srj_op* op, const double* x, const double* b,

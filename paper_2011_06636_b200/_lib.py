@@ -23,7 +23,8 @@ CYCLE_RAN, CYCLE_CONVERGED, CYCLE_DIVERGED = 0, 1, 2
 # Every symbol include/srj.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
     "srj_abi_version", "srj_last_error", "srj_op_create", "srj_op_destroy",
-    "srj_op_layout", "srj_op_diag", "srj_op_set_sweeps_per_pass", "srj_residual_sq",
+    "srj_op_layout", "srj_op_diag", "srj_op_set_sweeps_per_pass", "srj_op_describe",
+    "srj_residual_sq",
     "srj_run_cycle", "srj_sweep", "srj_matvec", "srj_fill_uniform_rhs",
 )
 
@@ -44,6 +45,15 @@ class CycleOut(ctypes.Structure):
     ]
 
 
+class OpInfo(ctypes.Structure):
+    _fields_ = [(name, c_int32) for name in (
+        "num_sms", "cycle_blocks", "cycle_threads", "sweeps_per_pass", "tb_supported",
+        "tb_blocks", "tb_occupancy", "tb_tiles")]
+
+    def as_dict(self):
+        return {name: int(getattr(self, name)) for name, _ in self._fields_}
+
+
 class SrjLibraryError(RuntimeError):
     pass
 
@@ -59,6 +69,7 @@ def _declare(L):
     L.srj_op_layout.argtypes = [c_void_p, POINTER(c_int64), POINTER(c_int64)]
     L.srj_op_diag.argtypes = [c_void_p, POINTER(c_double), POINTER(c_double)]
     L.srj_op_set_sweeps_per_pass.argtypes = [c_void_p, c_int32]
+    L.srj_op_describe.argtypes = [c_void_p, POINTER(OpInfo)]
     L.srj_residual_sq.argtypes = [c_void_p, c_void_p, c_void_p, POINTER(c_double), c_void_p]
     L.srj_run_cycle.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
                                 c_double, c_double, c_double, c_int64, c_void_p,

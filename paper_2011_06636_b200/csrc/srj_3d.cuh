@@ -1,0 +1,30 @@
+// Plane-streaming cycle kernel for the 3D 7-point stencil (declarations).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "srj_common.cuh"
+
+namespace srj {
+
+struct Plan3D {
+    bool supported = false;
+    int blocks = 0;     // cooperative grid
+    int per_sm = 0;     // resident CTAs per SM
+    int tiles_x = 0, tiles_y = 0;
+    int zc = 0;         // planes per work item
+    int nzc = 0;        // work items along z
+    int items = 0;
+};
+
+cudaError_t plan3d_init(Plan3D& plan, const Geom& g, int num_sms);
+
+// One cycle of M sweeps (M = 0: residual of x only).  Outputs as the other
+// cycle kernels: out_i = {executed, status, result buffer}, out_d = {sum r^2 of
+// the last residual evaluated, res_after}; hist[k] for k = 1..executed.
+cudaError_t launch3d_cycle(const Plan3D& plan, const Geom& g, double* x, double* x_alt,
+                           const double* b, const double* omegas, int M, double tol,
+                           double baseline, double* partials, double* hist, int* out_i,
+                           double* out_d, cudaStream_t st);
+
+}  // namespace srj

@@ -24,6 +24,7 @@
 #include "../../include/srj.h"
 #include "srj_common.cuh"
 #include "srj_stencil.cuh"
+#include "srj_3d.cuh"
 #include "srj_tb.cuh"
 #include "srj_walk.cuh"
 
@@ -162,6 +163,7 @@ struct srj_op {
     double* h_out_d = nullptr;
     double* h_hist = nullptr;
     TbPlan tb;                   // temporal-blocking plan (srj_tb.cuh)
+    Plan3D p3;                   // plane-streaming 3D plan (srj_3d.cuh)
 };
 
 template <int FAM>
@@ -269,6 +271,10 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("allocation failed: ") + cudaGetErrorString(e));
     }
+    if ((e = plan3d_init(op->p3, g, op->num_sms)) != cudaSuccess) {
+        srj_op_destroy(op);
+        return fail(SRJ_CUDA_ERROR, std::string("3D plan setup failed: ") + cudaGetErrorString(e));
+    }
     if ((e = tb_plan_init(op->tb, g, op->num_sms)) != cudaSuccess) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("temporal-blocking setup failed: ") + cudaGetErrorString(e));
@@ -309,6 +315,19 @@ int srj_op_diag(const srj_op* op, double* diag, double* inv_diag) {
     return SRJ_OK;
 }
 
+int srj_op_describe(const srj_op* op, srj_op_info* info) {
+    if (!op || !info) return fail(SRJ_BAD_ARGUMENT, "null argument");
+    info->num_sms = op->num_sms;
+    info->cycle_blocks = op->coop_blocks;
+    info->cycle_threads = op->coop_threads;
+    info->sweeps_per_pass = op->sweeps_per_pass;
+    info->tb_supported = op->tb.supported ? 1 : 0;
+    info->tb_blocks = op->tb.blocks[op->tb.small_variant];
+    info->tb_occupancy = op->tb.occupancy;
+    info->tb_tiles = op->tb.ntiles[op->tb.small_variant];
+    return SRJ_OK;
+}
+
 int srj_op_set_sweeps_per_pass(srj_op* op, int32_t s) {
     if (!op) return fail(SRJ_BAD_ARGUMENT, "null operator");
     if (s < 1 || s > kTbMaxSub) return fail(SRJ_BAD_ARGUMENT, "sweeps per pass out of range");
@@ -342,8 +361,13 @@ int srj_residual_sq(srj_op* op, const double* x, const double* b, double* sumsq_
     if (!op || !x || !b || !sumsq_host) return fail(SRJ_BAD_ARGUMENT, "null argument");
     DeviceGuard guard(op->device);
     cudaStream_t st = (cudaStream_t)stream;
-    int rc = launch_cycle(op, x, nullptr, b, nullptr, 0, 0.0, 1.0, st);
-    if (rc) return rc;
+    if (op->p3.supported) {
+        CUDA_TRY(launch3d_cycle(op->p3, op->g, const_cast<double*>(x), nullptr, b, nullptr, 0, 0.0,
+                                1.0, op->partials, op->hist, op->out_i, op->out_d, st));
+    } else {
+        int rc = launch_cycle(op, x, nullptr, b, nullptr, 0, 0.0, 1.0, st);
+        if (rc) return rc;
+    }
     CUDA_TRY(cudaMemcpyAsync(op->h_out_d, op->out_d, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     *sumsq_host = op->h_out_d[0];
@@ -372,7 +396,11 @@ int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
     const int Meff = (int)std::min<int64_t>(M, std::max<int64_t>(budget, 0));
     if (Meff == 0) return SRJ_OK;
 
-    if (op->sweeps_per_pass > 1 && op->tb.supported) {
+    if (op->p3.supported) {
+        CUDA_TRY(launch3d_cycle(op->p3, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,
+                                op->partials, op->hist, op->out_i, op->out_d, st));
+        out->launches = 1;
+    } else if (op->sweeps_per_pass > 1 && op->tb.supported) {
         CUDA_TRY(tb_launch_cycle(op->tb, op->g, x, x_alt, b, omegas_dev, Meff,
                                  op->sweeps_per_pass, tol, baseline, op->partials, op->hist,
                                  op->out_i, op->out_d, st));

@@ -12,11 +12,12 @@ constexpr int kTbMaxSub = 8;  // most sweeps fused into one pass
 
 struct TbPlan {
     bool supported = false;
-    int blocks = 0;      // cooperative grid (one CTA per SM)
-    int threads = 0;
-    size_t smem = 0;     // dynamic shared memory per CTA
-    int tiles_x = 0;
-    int ntiles = 0;
+    // per kernel variant (see srj_tb.cu, tb2d::Cfg<K>)
+    int blocks[4] = {0, 0, 0, 0};   // cooperative grid (one CTA per SM)
+    int tiles_x[4] = {0, 0, 0, 0};
+    int ntiles[4] = {0, 0, 0, 0};
+    int small_variant = 2;          // variant used for s <= 4
+    int occupancy = 0;              // min resident CTAs per SM over the variants
 };
 
 // Decide whether the operator has a temporal-blocking kernel and size its grid.

@@ -46,6 +46,16 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// 3D box load (x fastest, then y, then z planes).
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x0, int y0,
+                                            int z0, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(x0), "r"(y0), "r"(z0), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // Order prior generic-proxy accesses (st.global by other CTAs, made visible by
 // the grid barrier; ld.shared of the staging buffer by this CTA) before the
 // async-proxy TMA traffic that follows.
@@ -58,9 +68,17 @@ __device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)map) : "memory");
 }
 
+// Host: true when the driver exposes cuTensorMapEncodeTiled.
+bool tma_available();
+
 // Host: encode a 2D fp64 tensor map over an nx x ny field (row pitch nx) with
 // a box of box_x x box_y elements and zero fill out of bounds.
 cudaError_t encode_field_map(CUtensorMap* map, const double* base, int nx, int ny, int box_x,
                              int box_y);
+
+// Host: 3D fp64 map over nz planes of nx x ny (plane pitch nx*ny), box of
+// box_x x box_y x 1, zero fill out of bounds.
+cudaError_t encode_volume_map(CUtensorMap* map, const double* base, int nx, int ny, int nz,
+                              int box_x, int box_y);
 
 }  // namespace srj

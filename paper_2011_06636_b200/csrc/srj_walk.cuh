@@ -59,4 +59,40 @@ __device__ __forceinline__ double reduce_partials(const double* part, int nb, do
     return block_allsum(s, sh);
 }
 
+// Block sums of h <= H per-thread values at once (two barriers in total):
+// out[t] = sum over the block of v[t].  `sh` needs 32*H doubles, `out` H.
+template <int H>
+__device__ __forceinline__ void block_sums(const double (&v)[H], int h, double* sh, double* out) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int t = 0; t < H; ++t) {
+        if (t < h) {
+            const double s = warp_allsum(v[t]);
+            if (lane == 0) sh[wid * H + t] = s;
+        }
+    }
+    __syncthreads();
+    if (wid < h) {
+        double s = lane < nw ? sh[lane * H + wid] : 0.0;
+        s = warp_allsum(s);
+        if (lane == 0) out[wid] = s;
+    }
+    __syncthreads();
+}
+
+// out[t] = sum_q part[t*nb + q] for t < h (h <= warps per block), fixed order:
+// warp t strides over the nb partials, then a butterfly.  One barrier.
+__device__ __forceinline__ void reduce_partials_multi(const double* part, int nb, int h,
+                                                      double* out) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (wid < h) {
+        double s = 0.0;
+        for (int q = lane; q < nb; q += 32) s += __ldcg(part + wid * nb + q);
+        s = warp_allsum(s);
+        if (lane == 0) out[wid] = s;
+    }
+    __syncthreads();
+}
+
 }  // namespace srj

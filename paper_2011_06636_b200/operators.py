@@ -226,6 +226,12 @@ class StencilOperator:
         _lib.check(_lib.lib().srj_op_set_sweeps_per_pass(self.handle, int(s)),
                    "srj_op_set_sweeps_per_pass")
 
+    def describe(self) -> dict:
+        """Launch configuration libsrj chose for this operator."""
+        info = _lib.OpInfo()
+        _lib.check(_lib.lib().srj_op_describe(self.handle, ctypes.byref(info)), "srj_op_describe")
+        return info.as_dict()
+
     def new_field(self) -> Field:
         return Field(self.n, self.halo, self.device)
 

@@ -55,7 +55,7 @@ def main():
         us = ms * 1e3 / sch.M
         print(json.dumps({"case": spec, "M": sch.M, "spp": a.spp, "us_per_sweep": us,
                           "GBps_alg": bpu[fam] * A.n / (us * 1e-6) / 1e9,
-                          "GLUPs": A.n / (us * 1e-6) / 1e9, "launches": out.launches}),
+                          "GLUPs": A.n / (us * 1e-6) / 1e9, "launches": out.launches, "info": A.describe()}),
               flush=True)
 
 
