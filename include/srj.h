@@ -146,6 +146,22 @@ int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
 /* x_out = x + omega * inv_diag * (b - A x)  (one weighted Jacobi sweep). */
 int srj_sweep(srj_op* op, const double* x, double* x_out, const double* b,
               double omega, void* stream);
+/* Slab building blocks (multi-GPU decomposition).  The slab
+ * axis is z in 3D and y (rows) in 2D; a 1D operator is one plane.
+ * srj_op_planes: number of planes along the slab axis.
+ * srj_sweep_planes: one weighted-Jacobi sweep of planes [z_begin, z_end) from x
+ * into x_out (x_out == NULL: residual only) reading the ghost planes of x as
+ * they are; *partial_dev (device) = sum over those planes of (b - A x)^2, reduced
+ * in a fixed order.  Asynchronous; launches on the same `slot` (0 or 1) must
+ * not overlap, launches on different slots may run concurrently (e.g. interior
+ * planes while the halo exchange is in flight, then the boundary planes).
+ * Replaces, per slab: sparse.weighted_jacobi_sweep + the norm of
+ * solver.py:231-234. */
+int64_t srj_op_planes(const srj_op* op);
+int srj_sweep_planes(srj_op* op, const double* x, double* x_out, const double* b,
+                     double omega, int64_t z_begin, int64_t z_end, double* partial_dev,
+                     int32_t slot, void* stream);
+
 /* y = A x (y needs no ghosts). */
 int srj_matvec(srj_op* op, const double* x, double* y, void* stream);
 /* out[i] = 2 * u_{start+i} - 1, u_j the j-th uniform of SplitMix64(seed). */

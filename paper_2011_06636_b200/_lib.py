@@ -26,6 +26,7 @@ EXPORTED_SYMBOLS = (
     "srj_op_layout", "srj_op_diag", "srj_op_set_sweeps_per_pass", "srj_op_describe",
     "srj_residual_sq",
     "srj_run_cycle", "srj_sweep", "srj_matvec", "srj_fill_uniform_rhs",
+    "srj_op_planes", "srj_sweep_planes",
 )
 
 
@@ -77,9 +78,13 @@ def _declare(L):
     L.srj_sweep.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_void_p]
     L.srj_matvec.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p]
     L.srj_fill_uniform_rhs.argtypes = [c_void_p, c_int64, c_uint64, c_int64, c_int32, c_void_p]
+    L.srj_op_planes.argtypes = [c_void_p]
+    L.srj_sweep_planes.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int64,
+                                   c_int64, c_void_p, c_int32, c_void_p]
     for name in EXPORTED_SYMBOLS:
         if name not in ("srj_abi_version", "srj_last_error"):
             getattr(L, name).restype = c_int32
+    L.srj_op_planes.restype = c_int64
 
 
 def load(path: str = LIB_PATH):

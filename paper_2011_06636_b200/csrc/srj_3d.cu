@@ -53,6 +53,7 @@ struct Args3D {
     int* out_i;
     double* out_d;
     int tiles_x, ntiles, zc, items;
+    int zbase, zend;  // planes [zbase, zend) are swept (whole slab for a cycle)
 };
 
 struct Ring3D {
@@ -102,14 +103,14 @@ __device__ __forceinline__ double sweep3d(const Args3D& a, const CUtensorMap* mx
     using namespace k3;
     const int tid = threadIdx.x;
     const int tx = tid % TX, ty0 = tid / TX;
-    const int nx = a.g.nx, ny = a.g.ny, nz = a.g.nz;
+    const int nx = a.g.nx, ny = a.g.ny;
     const long long plane = (long long)nx * ny;
     const double coff = a.g.c_off, cdiag = a.g.c_diag, inv = a.g.inv_diag;
     double acc = 0.0;
     for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
         const int tile = item % a.ntiles, zci = item / a.ntiles;
         const int ox = (tile % a.tiles_x) * TX, oy = (tile / a.tiles_x) * TY;
-        const int z0 = zci * a.zc, z1 = min(z0 + a.zc, nz);
+        const int z0 = a.zbase + zci * a.zc, z1 = min(z0 + a.zc, a.zend);
         if (tid == 0) {
             for (int z = z0 - 1; z <= min(z0 + 2, z1); ++z) issue_x(mx, r, ox, oy, z);
             for (int z = z0; z <= min(z0 + 1, z1 - 1); ++z) issue_b(mb, r, ox, oy, z);
@@ -209,6 +210,34 @@ __global__ void __launch_bounds__(k3::THREADS) k_cycle3d(const __grid_constant__
     }
 }
 
+// One sweep (or residual, xout == nullptr) of planes [a.zbase, a.zend), the
+// building block of the slab-decomposed solve: *result receives the planes'
+// sum of r^2 (per-CTA partials reduced in a fixed order by the last CTA).
+__global__ void __launch_bounds__(k3::THREADS) k_sweep3d(const __grid_constant__ CUtensorMap mx,
+                                                         const __grid_constant__ CUtensorMap mb,
+                                                         Args3D a, double* xout, double w,
+                                                         double* block_part, unsigned* counter,
+                                                         double* result) {
+    using namespace k3;
+    extern __shared__ __align__(128) double smem[];
+    __shared__ double sh[32];
+    Ring3D r;
+    r.xs = smem;
+    r.bs = smem + XST * XPL;
+    r.xbar = reinterpret_cast<uint64_t*>(r.bs + BST * BPL);
+    r.bbar = r.xbar + XST;
+    r.xphase = 0;
+    r.bphase = 0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < XST; ++s) mbar_init(r.xbar + s, 1);
+        for (int s = 0; s < BST; ++s) mbar_init(r.bbar + s, 1);
+    }
+    __syncthreads();
+    double acc = xout ? sweep3d<true>(a, &mx, &mb, xout, w, r)
+                      : sweep3d<false>(a, &mx, &mb, nullptr, 0.0, r);
+    last_block_sum(acc, block_part, counter, result, sh);
+}
+
 cudaError_t plan3d_init(Plan3D& plan, const Geom& g, int num_sms) {
     plan = Plan3D();
     // TMA: 16-byte row pitch (even nx); tiles cover the grid in x/y
@@ -216,33 +245,66 @@ cudaError_t plan3d_init(Plan3D& plan, const Geom& g, int num_sms) {
     cudaError_t e = cudaFuncSetAttribute(k_cycle3d, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)k3::SMEM);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_sweep3d, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)k3::SMEM);
+    if (e != cudaSuccess) return e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cycle3d, k3::THREADS, k3::SMEM);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaSuccess;
     plan.per_sm = per_sm;
+    plan.slots = per_sm * num_sms;
     plan.tiles_x = (g.nx + k3::TX - 1) / k3::TX;
     plan.tiles_y = (g.ny + k3::TY - 1) / k3::TY;
-    const int ntiles = plan.tiles_x * plan.tiles_y;
-    const int slots = per_sm * num_sms;
-    // planes per item: minimise the critical path ceil(items/slots)*zc plus a
-    // two-plane pipeline fill per item
-    int best_zc = g.nz;
-    double best = 1e300;
-    for (int zc = 8; zc <= std::max(8, g.nz); zc += 8) {
-        const int nzc = (g.nz + zc - 1) / zc;
-        const long long items = (long long)ntiles * nzc;
-        const long long rounds = (items + slots - 1) / slots;
-        const double cost = (double)rounds * (zc + 2);
-        if (cost < best) { best = cost; best_zc = zc; }
-        if (zc >= g.nz) break;
-    }
-    plan.zc = std::min(best_zc, g.nz);
+    plan.zc = choose_zc(plan, g.nz);
     plan.nzc = (g.nz + plan.zc - 1) / plan.zc;
-    plan.items = ntiles * plan.nzc;
-    plan.blocks = std::max(1, std::min(slots, plan.items));
+    plan.items = plan.tiles_x * plan.tiles_y * plan.nzc;
+    plan.blocks = std::max(1, std::min(plan.slots, plan.items));
     plan.supported = true;
     return cudaSuccess;
+}
+
+// Planes per work item over a run of nzr planes: minimise the critical path
+// ceil(items/slots)*zc plus a two-plane pipeline fill per item.
+int choose_zc(const Plan3D& plan, int nzr) {
+    const int ntiles = plan.tiles_x * plan.tiles_y;
+    int best_zc = nzr;
+    double best = 1e300;
+    for (int zc = 8; zc <= std::max(8, nzr); zc += 8) {
+        const int nzc = (nzr + zc - 1) / zc;
+        const long long items = (long long)ntiles * nzc;
+        const long long rounds = (items + plan.slots - 1) / plan.slots;
+        const double cost = (double)rounds * (zc + 2);
+        if (cost < best) { best = cost; best_zc = zc; }
+        if (zc >= nzr) break;
+    }
+    return std::max(1, std::min(best_zc, nzr));
+}
+
+cudaError_t launch3d_sweep(const Plan3D& plan, const Geom& g, const double* x, double* x_out,
+                           const double* b, double omega, int z_begin, int z_end,
+                           double* block_part, unsigned* counter, double* result,
+                           cudaStream_t st) {
+    if ((((uintptr_t)x | (uintptr_t)b) & 15) != 0) return cudaErrorMisalignedAddress;
+    const long long plane = (long long)g.nx * g.ny;
+    CUtensorMap mx, mb;
+    cudaError_t e;
+    if ((e = encode_volume_map(&mx, x - plane, g.nx, g.ny, g.nz + 2, k3::BX, k3::BY)) != cudaSuccess)
+        return e;
+    if ((e = encode_volume_map(&mb, b, g.nx, g.ny, g.nz, k3::TX, k3::TY)) != cudaSuccess) return e;
+    Args3D a = {};
+    a.g = g;
+    a.tiles_x = plan.tiles_x;
+    a.ntiles = plan.tiles_x * plan.tiles_y;
+    const int nzr = z_end - z_begin;
+    a.zc = choose_zc(plan, nzr);
+    a.items = a.ntiles * ((nzr + a.zc - 1) / a.zc);
+    a.zbase = z_begin;
+    a.zend = z_end;
+    const int blocks = std::max(1, std::min(plan.slots, a.items));
+    k_sweep3d<<<blocks, k3::THREADS, k3::SMEM, st>>>(mx, mb, a, x_out, omega, block_part, counter,
+                                                     result);
+    return cudaGetLastError();
 }
 
 cudaError_t launch3d_cycle(const Plan3D& plan, const Geom& g, double* x, double* x_alt,
@@ -278,6 +340,8 @@ cudaError_t launch3d_cycle(const Plan3D& plan, const Geom& g, double* x, double*
     a.ntiles = plan.tiles_x * plan.tiles_y;
     a.zc = plan.zc;
     a.items = plan.items;
+    a.zbase = 0;
+    a.zend = g.nz;
     void* args[] = {&m0, &m1, &mb, &a};
     return cudaLaunchCooperativeKernel((const void*)k_cycle3d, dim3(plan.blocks),
                                        dim3(k3::THREADS), args, k3::SMEM, st);

@@ -15,9 +15,19 @@ struct Plan3D {
     int zc = 0;         // planes per work item
     int nzc = 0;        // work items along z
     int items = 0;
+    int slots = 0;      // resident CTAs over the whole GPU
 };
 
 cudaError_t plan3d_init(Plan3D& plan, const Geom& g, int num_sms);
+int choose_zc(const Plan3D& plan, int nzr);
+
+// One sweep (x_out != nullptr) or residual evaluation of planes
+// [z_begin, z_end); *result (device) = sum of r^2 over them.  block_part needs
+// plan.slots doubles, counter one zeroed unsigned (left zeroed on exit).
+cudaError_t launch3d_sweep(const Plan3D& plan, const Geom& g, const double* x, double* x_out,
+                           const double* b, double omega, int z_begin, int z_end,
+                           double* block_part, unsigned* counter, double* result,
+                           cudaStream_t st);
 
 // One cycle of M sweeps (M = 0: residual of x only).  Outputs as the other
 // cycle kernels: out_i = {executed, status, result buffer}, out_d = {sum r^2 of

@@ -36,6 +36,8 @@ constexpr int kMaxSchemeLength = 10000;  // reference schemes.py:24
 constexpr int kThreads = 256;       // standalone sweep / matvec kernels
 constexpr int kCoopThreads = 512;   // persistent cycle kernel: 2 CTAs per SM
 constexpr int kSmallThreads = 1024;
+constexpr int kSlots = 2;           // srj_sweep_planes scratch slots
+constexpr int kApplyBlocksPerSm = 16;  // grid cap of the non-persistent kernels
 constexpr long long kSmallUnits = 256;   // <= 8192 points: one CTA, no grid barrier
 
 struct CycleArgs {
@@ -96,6 +98,21 @@ __global__ void __launch_bounds__(kThreads) k_apply(Geom g, const double* x, dou
     const int u0 = (int)((long long)g.units * blockIdx.x / nb);
     const int u1 = (int)((long long)g.units * (blockIdx.x + 1) / nb);
     walk_units<FAM, MODE>(g, x, out, b, w, u0, u1);
+}
+
+// One sweep / residual over units [ub, ue) (whole x-rows of a plane range)
+// with the grid's sum of r^2 reduced into *result.
+template <int FAM, int MODE>
+__global__ void __launch_bounds__(kThreads) k_apply_range(Geom g, const double* x, double* out,
+                                                          const double* __restrict__ b, double w,
+                                                          int ub, int ue, double* block_part,
+                                                          unsigned* counter, double* result) {
+    __shared__ double sh[32];
+    const int nb = gridDim.x;
+    const int u0 = ub + (int)((long long)(ue - ub) * blockIdx.x / nb);
+    const int u1 = ub + (int)((long long)(ue - ub) * (blockIdx.x + 1) / nb);
+    const double acc = walk_units<FAM, MODE>(g, x, out, b, w, u0, u1);
+    last_block_sum(acc, block_part, counter, result, sh);
 }
 
 // SplitMix64 counter form: draw i of a stream seeded with s is
@@ -164,6 +181,10 @@ struct srj_op {
     double* h_hist = nullptr;
     TbPlan tb;                   // temporal-blocking plan (srj_tb.cuh)
     Plan3D p3;                   // plane-streaming 3D plan (srj_3d.cuh)
+    // srj_sweep_planes scratch, one set per slot (concurrent launches)
+    double* slot_part[kSlots] = {nullptr, nullptr};
+    unsigned* slot_counter = nullptr;  // device [kSlots], zero between launches
+    int slot_capacity = 0;             // doubles per slot_part
 };
 
 template <int FAM>
@@ -253,9 +274,11 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
         int per_sm = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cycle_kernel_for(g.fam), kCoopThreads, 0);
         if (e != cudaSuccess || per_sm < 1) { delete op; return fail(SRJ_CUDA_ERROR, "occupancy query failed"); }
-        // Few, fat CTAs: the per-sweep grid barrier and partial reduction cost
-        // grows with the CTA count.
-        long long want = (long long)std::min(per_sm, 2) * op->num_sms;
+        // Few, fat CTAs on mid-size grids (the per-sweep grid barrier and
+        // partial reduction cost grows with the CTA count); full occupancy on
+        // large, bandwidth-bound grids.
+        const bool large = g.units >= (1 << 16);
+        long long want = (long long)(large ? per_sm : std::min(per_sm, 2)) * op->num_sms;
         const long long cap = std::max<long long>(1, g.units / (4 * (kCoopThreads / 32)));
         op->coop_blocks = (int)std::min(want, cap);
         op->coop_threads = kCoopThreads;
@@ -282,6 +305,18 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
     // Default: 4 sweeps per pass where a temporally blocked kernel exists
     // (measured best on B200 for 2D), else one per pass.
     op->sweeps_per_pass = op->tb.supported ? 4 : 1;
+    op->slot_capacity = std::max(op->p3.slots, kApplyBlocksPerSm * op->num_sms);
+    for (int s = 0; s < kSlots; ++s) {
+        if ((e = cudaMalloc(&op->slot_part[s], op->slot_capacity * sizeof(double))) != cudaSuccess) {
+            srj_op_destroy(op);
+            return fail(SRJ_CUDA_ERROR, std::string("allocation failed: ") + cudaGetErrorString(e));
+        }
+    }
+    if ((e = cudaMalloc(&op->slot_counter, kSlots * sizeof(unsigned))) != cudaSuccess ||
+        (e = cudaMemset(op->slot_counter, 0, kSlots * sizeof(unsigned))) != cudaSuccess) {
+        srj_op_destroy(op);
+        return fail(SRJ_CUDA_ERROR, std::string("allocation failed: ") + cudaGetErrorString(e));
+    }
     *out = op;
     return SRJ_OK;
 }
@@ -296,6 +331,8 @@ int srj_op_destroy(srj_op* op) {
     cudaFreeHost(op->h_out_i);
     cudaFreeHost(op->h_out_d);
     cudaFreeHost(op->h_hist);
+    for (int s = 0; s < kSlots; ++s) cudaFree(op->slot_part[s]);
+    cudaFree(op->slot_counter);
     delete op;
     return SRJ_OK;
 }
@@ -436,6 +473,53 @@ int srj_matvec(srj_op* op, const double* x, double* y, void* stream) {
     if (!op || !x || !y) return fail(SRJ_BAD_ARGUMENT, "null argument");
     DeviceGuard guard(op->device);
     return launch_apply<kMatvec>(op, x, y, nullptr, 0.0, (cudaStream_t)stream);
+}
+
+int64_t srj_op_planes(const srj_op* op) {
+    if (!op) return -1;
+    return op->g.fam == F3D ? op->g.nz : (op->g.fam == F1D ? 1 : op->g.ny);
+}
+
+int srj_sweep_planes(srj_op* op, const double* x, double* x_out, const double* b, double omega,
+                     int64_t z_begin, int64_t z_end, double* partial_dev, int32_t slot,
+                     void* stream) {
+    if (!op || !x || !b || !partial_dev) return fail(SRJ_BAD_ARGUMENT, "null argument");
+    if (slot < 0 || slot >= kSlots) return fail(SRJ_BAD_ARGUMENT, "slot out of range");
+    const int64_t planes = srj_op_planes(op);
+    if (z_begin < 0 || z_end > planes || z_begin >= z_end)
+        return fail(SRJ_BAD_ARGUMENT, "plane range out of bounds");
+    DeviceGuard guard(op->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const Geom& g = op->g;
+    if (g.fam == F3D && op->p3.supported) {
+        CUDA_TRY(launch3d_sweep(op->p3, g, x, x_out, b, omega, (int)z_begin, (int)z_end,
+                                op->slot_part[slot], op->slot_counter + slot, partial_dev, st));
+        return SRJ_OK;
+    }
+    const long long rows_per_plane = g.fam == F3D ? g.ny : (g.fam == F1D ? 1 : 1);
+    const long long per_plane = (g.fam == F1D ? 1 : rows_per_plane) * g.upr;
+    const int ub = (int)(z_begin * (g.fam == F1D ? g.units : per_plane));
+    const int ue = (int)(z_end * (g.fam == F1D ? g.units : per_plane));
+    const int blocks = (int)std::max<long long>(
+        1, std::min<long long>((ue - ub + 7) / 8, (long long)kApplyBlocksPerSm * op->num_sms));
+    double* bp = op->slot_part[slot];
+    unsigned* ct = op->slot_counter + slot;
+#define SRJ_RANGE(FAM)                                                                          \
+    if (x_out)                                                                                  \
+        k_apply_range<FAM, kSweep><<<blocks, kThreads, 0, st>>>(g, x, x_out, b, omega, ub, ue,  \
+                                                                bp, ct, partial_dev);           \
+    else                                                                                        \
+        k_apply_range<FAM, kResid><<<blocks, kThreads, 0, st>>>(g, x, nullptr, b, 0.0, ub, ue,  \
+                                                                bp, ct, partial_dev);
+    switch (g.fam) {
+        case F1D: SRJ_RANGE(F1D) break;
+        case F2D: SRJ_RANGE(F2D) break;
+        case F3D: SRJ_RANGE(F3D) break;
+        default: SRJ_RANGE(F2DV) break;
+    }
+#undef SRJ_RANGE
+    CUDA_TRY(cudaGetLastError());
+    return SRJ_OK;
 }
 
 int srj_fill_uniform_rhs(double* out, int64_t n, uint64_t seed, int64_t start, int32_t device,

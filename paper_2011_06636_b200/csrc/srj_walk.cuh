@@ -59,6 +59,30 @@ __device__ __forceinline__ double reduce_partials(const double* part, int nb, do
     return block_allsum(s, sh);
 }
 
+// Non-cooperative grid sum: every CTA contributes `acc`; the last CTA to
+// arrive reduces the per-CTA values in a fixed order into *result and re-arms
+// the counter (threadfence-reduction pattern).
+__device__ __forceinline__ void last_block_sum(double acc, double* block_part, unsigned* counter,
+                                               double* result, double* sh) {
+    __shared__ int s_last;
+    acc = block_allsum(acc, sh);
+    if (threadIdx.x == 0) {
+        block_part[blockIdx.x] = acc;
+        __threadfence();
+        const unsigned ticket = atomicAdd(counter, 1u);
+        s_last = ticket == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        const double s = reduce_partials(block_part, gridDim.x, sh);
+        if (threadIdx.x == 0) {
+            *result = s;
+            *counter = 0u;
+        }
+    }
+}
+
 // Block sums of h <= H per-thread values at once (two barriers in total):
 // out[t] = sum over the block of v[t].  `sh` needs 32*H doubles, `out` H.
 template <int H>

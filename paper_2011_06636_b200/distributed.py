@@ -1,0 +1,430 @@
+"""Slab-decomposed SRJ solve: one z-slab (3D) or row-slab (2D) per GPU.
+
+The reference has no parallelism beyond a process pool of independent runs
+(reference cli.py:196-198); this module is the multi-GPU form of the same
+solve.  Each rank owns `count` consecutive planes of the global
+grid in a Field whose ghost planes hold the neighbours' boundary planes (zero
+on a Dirichlet face), so every per-point computation -- and therefore every
+iterate -- is bit-identical to the single-GPU solve.
+
+Protocol per cycle (M sweeps, identical on every rank):
+  0. snapshot x_0 (device copy, 16 B/point once per cycle);
+  1. for each sweep k: exchange ghost planes of x_k with the z-/y-neighbours
+     (overlapped with the interior planes' sweep), sweep the boundary planes,
+     record the slab's sum of (b - A x_k)^2 -- three deterministic device
+     partials (interior, low face, high face);
+  2. residual of x_M (same exchange);
+  3. ONE all-gather of the (M+1) x 3 partials; every rank sums them in rank
+     order -- bit-identical global norms everywhere -- and applies the
+     reference's per-sweep stopping rule (solver.py:216-222,235-239) to
+     res_1 .. res_M;
+  4. a stop at sweep k < M restores the snapshot and re-runs k sweeps.
+So the data path has one ghost-plane exchange per sweep and one small
+collective per cycle; the host reads one gathered vector per cycle.
+
+Exchangers: `TorchExchanger` (one slab per process; torch.distributed P2P --
+NCCL over NVLink between GPUs, gloo on CPU for the tests) and
+`LocalExchanger` (several slabs in one process, e.g. virtual ranks on one GPU,
+exchanging by device copies).  Engines: `DeviceEngine` (libsrj's
+srj_sweep_planes) or any object with the same `apply` method (the CPU tests
+plug in a numpy engine).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .operators import Field, StencilOperator, fill_uniform_rhs
+from .problems import ABSOLUTE_L2, RELATIVE_L2
+from .schemes import MAX_LEVEL, ORDER_GRID_SIZE
+from .solver import (CycleStats, Heuristic, Increasing, SolveDivergedError, SolveReport,
+                     SolverState, StoppingRule, _l2_norm_parts, _next_scheme,
+                     average_convergence_rate, heuristic_next_level)
+
+PARTS = 3  # interior planes, low face, high face
+
+
+def _torch():
+    import torch
+    return torch
+
+
+# ---------------------------------------------------------------------------
+# Layout
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class SlabLayout:
+    """Global grid split into `world` slabs of whole planes along the slowest
+    axis (z in 3D, y in 2D); slab sizes differ by at most one plane."""
+
+    family: str
+    shape: tuple
+    world: int
+
+    def __post_init__(self):
+        if self.family == "1d3" and self.world != 1:
+            raise ValueError("a 1D grid is not sharded (replicas only)")
+        if self.world < 1 or self.world > self.planes:
+            raise ValueError(f"{self.world} slabs for {self.planes} planes")
+
+    @property
+    def planes(self) -> int:
+        return 1 if self.family == "1d3" else int(self.shape[-1])
+
+    @property
+    def plane_points(self) -> int:
+        return int(np.prod(self.shape[:-1])) if self.family != "1d3" else int(self.shape[0])
+
+    @property
+    def n(self) -> int:
+        return int(np.prod(self.shape))
+
+    def span(self, rank: int) -> tuple[int, int]:
+        base, extra = divmod(self.planes, self.world)
+        count = base + (1 if rank < extra else 0)
+        start = rank * base + min(rank, extra)
+        return start, count
+
+    def local_shape(self, rank: int) -> tuple:
+        if self.family == "1d3":
+            return tuple(self.shape)
+        return tuple(self.shape[:-1]) + (self.span(rank)[1],)
+
+
+class Slab:
+    """One rank's planes: operator, right-hand side, iterate, ping-pong partner
+    and the cycle-start snapshot (all Fields with ghost planes)."""
+
+    def __init__(self, layout: SlabLayout, rank: int, device, dx2: float | None = None,
+                 face_x=None, face_y=None):
+        self.layout = layout
+        self.rank = rank
+        self.start, self.count = layout.span(rank)
+        nx = layout.shape[0]
+        if dx2 is None and layout.family != "2d5var":
+            dx2 = (nx + 1.0) ** 2
+        if layout.family == "2d5var":
+            fx = face_x[self.start:self.start + self.count, :]
+            fy = face_y[self.start:self.start + self.count + 1, :]
+            self.A = StencilOperator("2d5var", layout.local_shape(rank), face_x=fx, face_y=fy,
+                                     device=device)
+        else:
+            self.A = StencilOperator(layout.family, layout.local_shape(rank), dx2=dx2,
+                                     device=device)
+        self.device = device
+        self.x = self.A.new_field()
+        self.x_alt = self.A.new_field()
+        self.snap = self.A.new_field()
+        self.b = self.A.new_field()
+
+    @property
+    def offset(self) -> int:
+        """Global flat index of the slab's first interior point."""
+        return self.start * self.layout.plane_points
+
+    @property
+    def planes(self) -> int:
+        return self.count if self.layout.family != "1d3" else 1
+
+    def swap(self) -> None:
+        self.x, self.x_alt = self.x_alt, self.x
+
+
+def _plane(field: Field, which: str):
+    """Views of a Field: 'lo_ghost', 'first', 'last', 'hi_ghost'."""
+    h, n = field.halo, field.n
+    buf = field.buf
+    return {"lo_ghost": buf[0:h], "first": buf[h:2 * h], "last": buf[n:n + h],
+            "hi_ghost": buf[n + h:n + 2 * h]}[which]
+
+
+# ---------------------------------------------------------------------------
+# Exchangers
+# ---------------------------------------------------------------------------
+
+class LocalExchanger:
+    """All slabs live in this process (virtual ranks): ghost planes are filled
+    by device copies; the gather is a stack."""
+
+    def __init__(self, world: int):
+        self.world = world
+
+    def start(self, fields):
+        for lo, hi in zip(fields[:-1], fields[1:]):
+            _plane(hi, "lo_ghost").copy_(_plane(lo, "last"))
+            _plane(lo, "hi_ghost").copy_(_plane(hi, "first"))
+        return None
+
+    def finish(self, handle) -> None:
+        return None
+
+    def exchange(self, fields) -> None:
+        self.finish(self.start(fields))
+
+    def allgather(self, tensors):
+        torch = _torch()
+        dev = tensors[0].device
+        return torch.stack([t.to(dev) for t in tensors])
+
+
+class TorchExchanger:
+    """One slab per process; torch.distributed point-to-point for the ghost
+    planes (NCCL over NVLink/NVSwitch on GPUs, gloo on CPU) and all_gather for
+    the per-cycle partials."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def start(self, fields):
+        (f,) = fields
+        dist = self.dist
+        ops = []
+        if self.rank > 0:
+            ops.append(dist.P2POp(dist.isend, _plane(f, "first"), self.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, _plane(f, "lo_ghost"), self.rank - 1, self.group))
+        if self.rank < self.world - 1:
+            ops.append(dist.P2POp(dist.isend, _plane(f, "last"), self.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, _plane(f, "hi_ghost"), self.rank + 1, self.group))
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def finish(self, reqs) -> None:
+        for r in reqs:
+            r.wait()
+
+    def exchange(self, fields) -> None:
+        self.finish(self.start(fields))
+
+    def allgather(self, tensors):
+        torch = _torch()
+        (t,) = tensors
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return torch.stack(out)
+
+
+# ---------------------------------------------------------------------------
+# Engines
+# ---------------------------------------------------------------------------
+
+class DeviceEngine:
+    """libsrj slab kernels: srj_sweep_planes (sum of r^2 written on device)."""
+
+    overlap = True
+
+    def apply(self, slab: Slab, xin: Field, xout: Field | None, w: float, z0: int, z1: int,
+              out, slot: int) -> None:
+        slab.A.sweep_planes(xin, xout, slab.b, w, z0, z1, out.data_ptr(), slot)
+
+
+# ---------------------------------------------------------------------------
+# Solver
+# ---------------------------------------------------------------------------
+
+class SlabSolver:
+    """`solve` over slabs (drop-in semantics of reference solver.py:289-331)."""
+
+    def __init__(self, slabs: list[Slab], exchanger, engine=None):
+        if not slabs:
+            raise ValueError("no slabs")
+        self.slabs = slabs
+        self.ex = exchanger
+        self.engine = engine if engine is not None else DeviceEngine()
+        self.layout = slabs[0].layout
+        self._parts = None
+
+    # -- data ---------------------------------------------------------------
+    def load(self, b=None, x0=None, seed: int | None = None) -> None:
+        """b: global numpy vector (sliced per slab) or None with `seed` for the
+        SplitMix64 right-hand side generated in place on each slab's device;
+        x0: global numpy vector or None (zero)."""
+        for s in self.slabs:
+            lo, hi = s.offset, s.offset + s.A.n
+            if b is not None:
+                s.b.copy_(np.asarray(b)[lo:hi])
+            elif seed is not None and s.b.device.type == "cuda":
+                fill_uniform_rhs(s.b, seed, start=lo)
+            elif seed is not None:
+                from .rng import uniforms_counter
+                s.b.copy_(2.0 * uniforms_counter(seed, hi - lo, start=lo) - 1.0)
+            else:
+                raise ValueError("need b or seed")
+            s.x.buf.zero_()
+            s.x_alt.buf.zero_()
+            if x0 is not None:
+                s.x.copy_(np.asarray(x0)[lo:hi])
+
+    def gather(self) -> np.ndarray:
+        """The global iterate on the host (tests and small problems)."""
+        torch = _torch()
+        parts = self.ex.allgather([self._padded_interior(s) for s in self.slabs])
+        total = []
+        for r in range(self.layout.world):
+            start, count = self.layout.span(r)
+            total.append(parts[r][:count * self.layout.plane_points].cpu().numpy())
+        del torch
+        return np.concatenate(total)
+
+    def _padded_interior(self, s: Slab):
+        torch = _torch()
+        base, extra = divmod(self.layout.planes, self.layout.world)
+        size = (base + (1 if extra else 0)) * self.layout.plane_points
+        out = torch.zeros(size, dtype=torch.float64, device=s.x.buf.device)
+        out[:s.A.n].copy_(s.x.interior)
+        return out
+
+    # -- kernels over all local slabs ----------------------------------------
+    def _parts_buffer(self, K: int):
+        torch = _torch()
+        return [torch.zeros((K, PARTS), dtype=torch.float64, device=s.x.buf.device)
+                for s in self.slabs]
+
+    def _sweep(self, w: float, parts, k: int) -> None:
+        eng = self.engine
+        P = [s.planes for s in self.slabs]
+        if getattr(eng, "overlap", False) and min(P) >= 3:
+            handle = self.ex.start([s.x for s in self.slabs])
+            for s, p in zip(self.slabs, parts):
+                eng.apply(s, s.x, s.x_alt, w, 1, s.planes - 1, p[k, 0], 0)
+            self.ex.finish(handle)
+            for s, p in zip(self.slabs, parts):
+                eng.apply(s, s.x, s.x_alt, w, 0, 1, p[k, 1], 1)
+                eng.apply(s, s.x, s.x_alt, w, s.planes - 1, s.planes, p[k, 2], 1)
+        else:
+            self.ex.exchange([s.x for s in self.slabs])
+            for s, p in zip(self.slabs, parts):
+                eng.apply(s, s.x, s.x_alt, w, 0, s.planes, p[k, 0], 0)
+        for s in self.slabs:
+            s.swap()
+
+    def _residual(self, parts, k: int) -> None:
+        self.ex.exchange([s.x for s in self.slabs])
+        for s, p in zip(self.slabs, parts):
+            self.engine.apply(s, s.x, None, 0.0, 0, s.planes, p[k, 0], 0)
+
+    def _global_sums(self, parts, K: int) -> np.ndarray:
+        g = self.ex.allgather(parts).cpu().numpy()  # [world, K, PARTS]
+        acc = np.zeros(K)
+        for r in range(g.shape[0]):  # fixed rank order: identical bits on every rank
+            acc = acc + ((g[r, :K, 0] + g[r, :K, 1]) + g[r, :K, 2])
+        return acc
+
+    def residual_norm(self) -> float:
+        parts = self._parts_buffer(1)
+        self._residual(parts, 0)
+        return math.sqrt(self._global_sums(parts, 1)[0])
+
+    # -- cycle / solve ----------------------------------------------------------
+    def cycle(self, ordered_omegas, res_before: float, tol: float, baseline: float,
+              budget: int):
+        """Returns (executed, status, res_after, history[1..executed])."""
+        M = len(ordered_omegas)
+        if res_before <= tol:
+            return 0, "converged", res_before, []
+        Meff = min(M, max(budget, 0))
+        if Meff == 0:
+            return 0, "ran", res_before, []
+        for s in self.slabs:
+            s.snap.buf.copy_(s.x.buf)
+        parts = self._parts_buffer(Meff + 1)
+        for k in range(Meff):
+            self._sweep(ordered_omegas[k], parts, k)
+        self._residual(parts, Meff)
+        sums = self._global_sums(parts, Meff + 1)
+        res = np.sqrt(sums) / baseline
+        stop, status = None, "ran"
+        for k in range(1, Meff + 1):
+            if not math.isfinite(res[k]):
+                stop, status = k, "diverged"
+                break
+            if res[k] <= tol:
+                stop, status = k, "converged"
+                break
+        executed = Meff if stop is None else stop
+        if executed < Meff:
+            # roll back: x_executed from the cycle-start snapshot
+            for s in self.slabs:
+                s.x.buf.copy_(s.snap.buf)
+            scratch = self._parts_buffer(max(executed, 1))
+            for k in range(executed):
+                self._sweep(ordered_omegas[k], scratch, k)
+        return executed, status, float(res[executed]), [float(v) for v in res[1:executed + 1]]
+
+    def solve(self, controller, stopping: StoppingRule, order_grid: int = ORDER_GRID_SIZE,
+              record_history: bool = True) -> SolveReport:
+        t0 = time.perf_counter()
+        _l2_norm_parts(stopping.norm)
+        r0 = self.residual_norm()
+        baseline = 1.0
+        if stopping.norm == RELATIVE_L2:
+            baseline = r0
+            if baseline == 0.0:
+                raise ValueError("initial residual is zero; relative norm undefined")
+        res_now = r0 / baseline
+        state = SolverState(x=None, level=0)
+        history = [(0, res_now)] if record_history else []
+        cycles: list[CycleStats] = []
+        converged = False
+        while True:
+            scheme = _next_scheme(controller, state, order_grid)
+            ordered = scheme.ordered_omegas()
+            budget = stopping.max_iterations - state.total_iterations
+            res_before = res_now
+            executed, status, res_after, hist = self.cycle(
+                ordered, res_before, stopping.tolerance, baseline, budget)
+            if status == "diverged":
+                raise SolveDivergedError({
+                    "cycle": state.cycle_index, "sweep": executed,
+                    "omega": ordered[executed - 1], "level": scheme.level, "M": scheme.M})
+            if record_history:
+                history.extend((state.total_iterations + i + 1, r) for i, r in enumerate(hist))
+            res_now = res_after
+            if executed > 0 and res_before > 0.0 and res_after > 0.0:
+                rate = average_convergence_rate(res_before, res_after, executed)
+                ratio = res_after / res_before
+            else:
+                rate = math.inf if executed > 0 else 0.0
+                ratio = state.prev_residual_ratio
+            if executed > 0:
+                cycles.append(CycleStats(
+                    cycle=state.cycle_index,
+                    level=scheme.level if scheme.level is not None else -1, M=scheme.M,
+                    executed=executed, residual_before=res_before, residual_after=res_after,
+                    average_rate=rate))
+                state.prev_residual_ratio = ratio
+            state.level = scheme.level if scheme.level is not None else state.level
+            state.cycle_index += 1
+            state.total_iterations += executed
+            if res_now <= stopping.tolerance:
+                converged = True
+                break
+            if state.total_iterations >= stopping.max_iterations:
+                break
+            if isinstance(controller, Heuristic):
+                r = state.prev_residual_ratio
+                if r is not None and math.isfinite(r):
+                    state.level = heuristic_next_level(r, state.level, controller.t_hi,
+                                                       controller.t_lo)
+            elif isinstance(controller, Increasing):
+                state.level = min(state.level + 1, MAX_LEVEL)
+        return SolveReport(converged=converged, total_iterations=state.total_iterations,
+                           cycles=cycles, wall_time=time.perf_counter() - t0,
+                           x=[s.x.interior for s in self.slabs], residual_history=history)
+
+
+def local_slabs(family: str, shape, world: int, ranks, device, face_x=None, face_y=None,
+                dx2: float | None = None) -> list[Slab]:
+    layout = SlabLayout(family, tuple(shape), world)
+    return [Slab(layout, r, device, dx2=dx2, face_x=face_x, face_y=face_y) for r in ranks]
+
+
+__all__ = ["SlabLayout", "Slab", "LocalExchanger", "TorchExchanger", "DeviceEngine",
+           "SlabSolver", "local_slabs", "PARTS", "ABSOLUTE_L2"]

@@ -256,6 +256,21 @@ class StencilOperator:
                                         _stream_handle(self.device)), "srj_sweep")
         return out
 
+    def sweep_planes(self, x: Field, x_out: Field | None, b: Field, omega: float, z_begin: int,
+                     z_end: int, partial_ptr: int, slot: int = 0) -> None:
+        """Sweep (or residual, x_out None) of slab planes [z_begin, z_end);
+        the planes' sum of r^2 lands at device address `partial_ptr`."""
+        _lib.check(_lib.lib().srj_sweep_planes(
+            self.handle, x.ptr, x_out.ptr if x_out is not None else None, b.ptr, float(omega),
+            int(z_begin), int(z_end), ctypes.c_void_p(partial_ptr), int(slot),
+            _stream_handle(self.device)), "srj_sweep_planes")
+
+    @property
+    def planes(self) -> int:
+        """Planes along the slab axis (z in 3D, rows in 2D, 1 in 1D)."""
+        return {"1d3": 1, "2d5": self.shape[1], "2d5var": self.shape[1],
+                "3d7": self.shape[2]}[self.family]
+
     def matvec(self, x: Field):
         torch = _torch()
         y = torch.empty(self.n, dtype=torch.float64, device=self.device)
