@@ -38,6 +38,7 @@ CONFIG_DESC = {
     "c3": "3D Poisson 7-pt 512^3 Dirichlet, f~U[-1,1) SplitMix64, rel L2 1e-8, SRJ heuristic",
     "c1": "1D Poisson 3-pt N=1024 Dirichlet, f~U[-1,1) SplitMix64, rel L2 1e-8, SRJ heuristic",
     "c4": "2D var-coef 5-pt 4096^2 harmonic faces k=exp(g), rel L2 1e-8, SRJ heuristic",
+    "c5": "3D Poisson 7-pt 1024x1024x(128N) z-slabs over N GPUs, 50 heuristic cycles",
 }
 BYTES_PER_UPDATE = {"1d3": 24, "2d5": 24, "3d7": 24, "2d5var": 40}
 L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
@@ -56,6 +57,8 @@ def parse():
     ap.add_argument("--sweeps-per-pass", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--planes-per-gpu", type=int, default=128, help="c5: z planes per GPU")
+    ap.add_argument("--cycles", type=int, default=50, help="c5: heuristic cycles per step")
     return ap.parse_args()
 
 
@@ -123,12 +126,27 @@ def measured_peak():
 
 
 def traffic_from_profile(config):
+    """DRAM bytes (read + write) of one captured launch of the dominant kernel
+    from `ncu --set full` (profiles/traffic.json), with that launch's
+    algorithmic bytes for scale; None when no capture exists for the config."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(config)
+            entry = json.load(fh).get(config)
     except Exception:
         return None
+    if not entry:
+        return None
+    return {"traffic": entry["traffic"], "alg_bytes": entry["alg_bytes"],
+            "ratio": entry["traffic_over_alg"], "launch": entry["launch"]}
+
+
+def kernel_name(family, info):
+    if family == "3d7":
+        return "srj::k_cycle3d (TMA plane ring)"
+    if info.get("tb_supported") and info.get("sweeps_per_pass", 1) > 1:
+        return "srj::k_tb2d_cycle (TMA temporal blocking)"
+    return "srj::k_cycle"
 
 
 def cpu_sample(family, n, seed, budget_s):
@@ -137,7 +155,11 @@ def cpu_sample(family, n, seed, budget_s):
     import numpy as np
 
     from oracle import srj_oracle as O
-    op = O.stencil(family, n)
+    fx = fy = None
+    if family == "2d5var":
+        from paper_2011_06636_b200.problems import gaussian_field, harmonic_faces
+        fx, fy = harmonic_faces(np.exp(gaussian_field(n, seed)), (n + 1.0) ** 2)
+    op = O.stencil(family, n, fx=fx, fy=fy)
     b = O.uniform_rhs(seed, op.n)
     seq = O.scheme(O.LADDER[14])[0]
     x = np.zeros(op.n)
@@ -161,8 +183,11 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     from paper_2011_06636_b200.problems import CONFIGS
-    family, extent, _ = CONFIGS[args.config]
-    n = args.size or extent
+    if args.config == "c5":  # per-GPU load of config 5 = a 512^3 cube of points
+        family, n = "3d7", 512
+    else:
+        family, extent, _ = CONFIGS[args.config]
+        n = args.size or extent
     for _ in range(args.warmup):
         cpu_sample(family, n, args.seed, min(2.0, args.cpu_seconds))
     vals = []
@@ -184,6 +209,86 @@ def run_reference(args, rank, world):
         "e2e": {"value": v, "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def run_slabs(args, rank, world, local):
+    """Config 5 family: 3D Poisson z-slabs of nx x ny x planes_per_gpu on each of
+    N GPUs (N = 8: the 1024^3 grid of BASELINE config 5; N = 1: the 134M-point
+    per-GPU load of config 3), a fixed 50 heuristic cycles in throughput mode.
+    Halo planes go over NCCL (torch.distributed P2P) overlapped with the
+    interior planes' sweep; one all-gather of per-sweep partials per cycle."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2011_06636_b200 as srj
+    from paper_2011_06636_b200.distributed import (LocalExchanger, SlabSolver, TorchExchanger,
+                                                   local_slabs)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    nx = args.size or 1024
+    shape = (nx, nx, args.planes_per_gpu * world)
+    slabs = local_slabs("3d7", shape, world, [rank], dev)
+    ex = TorchExchanger() if world > 1 else LocalExchanger(1)
+    solver = SlabSolver(slabs, ex)
+    rule = srj.StoppingRule("relative_l2", 1e-300, 10**9)
+    ctrl = srj.Heuristic()
+    stream = torch.cuda.current_stream(dev)
+
+    def one():
+        solver.load(seed=args.seed)
+        return solver.solve(ctrl, rule, record_history=False, max_cycles=args.cycles)
+
+    for _ in range(args.warmup):
+        one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms, sweeps = [], []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rep = one()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            sweeps.append(rep.total_iterations)
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    n_global = int(np.prod(shape))
+    value = n_global * sum(sweeps) / (total_ms * 1e-3) / 1e9
+    per_gpu_bytes = 24.0 * slabs[0].A.n * sum(sweeps)
+    peak, peak_kind = measured_peak()
+    achieved = per_gpu_bytes / (total_ms * 1e-3) / 1e9
+    line = {
+        "metric": "GLUP/s (SRJ point-updates/s), 50 heuristic cycles (throughput mode)",
+        "value": value, "unit": "GLUP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (f = 2u-1 from SplitMix64(seed), generated per slab on device)",
+        "config": {"workload": f"3D Poisson 7-pt {shape[0]}x{shape[1]}x{shape[2]} z-slabs "
+                               f"({args.planes_per_gpu} planes/GPU), {args.cycles} cycles",
+                   "sweeps_per_step": sweeps[-1], "cycles": len(rep.cycles),
+                   "levels": [c.level for c in rep.cycles],
+                   "executed": [c.executed for c in rep.cycles],
+                   "parallelism": f"z-slabs x{world}, NCCL halo P2P overlapped"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "srj::k_sweep3d (slab sweep, whole step incl. exchange)"},
+        "clocks": clocks.summary(),
+        "gpu_launches": int(sum(sweeps) * 3 + len(rep.cycles) * 2),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def run_ours(args, rank, world, local):
@@ -278,7 +383,7 @@ def run_ours(args, rank, world, local):
 
     # e2e: public API with pinned host buffers, H2D + D2H inside the region
     b_host = torch.empty(A.n, dtype=torch.float64, pin_memory=True)
-    b_host.copy_(prob.b)
+    b_host.copy_(torch.as_tensor(prob.b))
     x0_host = torch.zeros(A.n, dtype=torch.float64, pin_memory=True)
     p_host = srj.ProblemInstance(A=A, b=b_host, x0=x0_host, stopping_norm="relative_l2")
     e2e_ms = []
@@ -294,6 +399,7 @@ def run_ours(args, rank, world, local):
         assert r2.total_iterations == rep.total_iterations
     e2e_val = A.n * sum(e2e_sweeps) / (sum(e2e_ms) * 1e-3) / 1e9
 
+    info = A.describe()
     peak, peak_kind = measured_peak()
     achieved = sum(launch_bytes) / (sum(launch_ms) * 1e-3) / 1e9 if launch_ms else None
     traffic = traffic_from_profile(args.config)
@@ -305,17 +411,23 @@ def run_ours(args, rank, world, local):
         "data": "synthetic (f = 2u-1, u from SplitMix64(seed) in index order; x0 = 0)",
         "config": {"workload": CONFIG_DESC[args.config], "grid": n, "n": A.n,
                    "sweeps_per_solve": sweeps[-1], "cycles_per_solve": len(rep.cycles),
-                   "levels_tail": [c.level for c in rep.cycles][-6:],
+                   "levels": [c.level for c in rep.cycles],
+                   "executed": [c.executed for c in rep.cycles],
                    "time_to_tolerance_ms": ms_per_step,
                    "l2": "flushed between steps (512 MiB write)",
-                   "sweeps_per_pass": args.sweeps_per_pass or 1,
+                   "sweeps_per_pass": info["sweeps_per_pass"] if info["tb_supported"] else 1,
+                   "launch": info,
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
         "e2e": {"value": e2e_val, "unit": "GLUP/s",
                 "h2d_bytes_per_step": 2 * 8 * A.n, "d2h_bytes_per_step": 8 * A.n,
                 "ms_per_step": sum(e2e_ms) / len(e2e_ms)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if achieved else None, "traffic": traffic,
-                     "peak_kind": peak_kind, "kernel": "srj::k_cycle",
+                     "frac": achieved / peak if achieved else None,
+                     "traffic": traffic["traffic"] if traffic else None,
+                     "traffic_launch_alg_bytes": traffic["alg_bytes"] if traffic else None,
+                     "traffic_over_alg": traffic["ratio"] if traffic else None,
+                     "traffic_launch": traffic["launch"] if traffic else None,
+                     "peak_kind": peak_kind, "kernel": kernel_name(family, info),
                      "bytes_per_update": bpu,
                      "launches_timed": len(launch_ms)},
         "clocks": clocks.summary(),
@@ -334,6 +446,9 @@ def main():
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.config == "c5":
+        run_slabs(args, rank, world, local)
         return
     run_ours(args, rank, world, local)
 

@@ -359,7 +359,9 @@ class SlabSolver:
         return executed, status, float(res[executed]), [float(v) for v in res[1:executed + 1]]
 
     def solve(self, controller, stopping: StoppingRule, order_grid: int = ORDER_GRID_SIZE,
-              record_history: bool = True) -> SolveReport:
+              record_history: bool = True, max_cycles: int | None = None) -> SolveReport:
+        """`max_cycles` caps the number of cycles (throughput mode, BASELINE
+        config 5: a fixed count of heuristic-selected cycles)."""
         t0 = time.perf_counter()
         _l2_norm_parts(stopping.norm)
         r0 = self.residual_norm()
@@ -407,6 +409,8 @@ class SlabSolver:
                 converged = True
                 break
             if state.total_iterations >= stopping.max_iterations:
+                break
+            if max_cycles is not None and state.cycle_index >= max_cycles:
                 break
             if isinstance(controller, Heuristic):
                 r = state.prev_residual_ratio
