@@ -24,6 +24,7 @@
 #include "../../include/srj.h"
 #include "srj_common.cuh"
 #include "srj_stencil.cuh"
+#include "srj_2d.cuh"
 #include "srj_3d.cuh"
 #include "srj_tb.cuh"
 #include "srj_walk.cuh"
@@ -181,6 +182,7 @@ struct srj_op {
     double* h_hist = nullptr;
     TbPlan tb;                   // temporal-blocking plan (srj_tb.cuh)
     Plan3D p3;                   // plane-streaming 3D plan (srj_3d.cuh)
+    Plan2D p2;                   // tile-streaming 2D plan (srj_2d.cuh)
     // srj_sweep_planes scratch, one set per slot (concurrent launches)
     double* slot_part[kSlots] = {nullptr, nullptr};
     unsigned* slot_counter = nullptr;  // device [kSlots], zero between launches
@@ -294,6 +296,10 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("allocation failed: ") + cudaGetErrorString(e));
     }
+    if ((e = plan2d_init(op->p2, g, op->num_sms)) != cudaSuccess) {
+        srj_op_destroy(op);
+        return fail(SRJ_CUDA_ERROR, std::string("2D plan setup failed: ") + cudaGetErrorString(e));
+    }
     if ((e = plan3d_init(op->p3, g, op->num_sms)) != cudaSuccess) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("3D plan setup failed: ") + cudaGetErrorString(e));
@@ -333,6 +339,7 @@ int srj_op_destroy(srj_op* op) {
     cudaFreeHost(op->h_hist);
     for (int s = 0; s < kSlots; ++s) cudaFree(op->slot_part[s]);
     cudaFree(op->slot_counter);
+    plan2d_free(op->p2);
     delete op;
     return SRJ_OK;
 }
@@ -401,6 +408,9 @@ int srj_residual_sq(srj_op* op, const double* x, const double* b, double* sumsq_
     if (op->p3.supported) {
         CUDA_TRY(launch3d_cycle(op->p3, op->g, const_cast<double*>(x), nullptr, b, nullptr, 0, 0.0,
                                 1.0, op->partials, op->hist, op->out_i, op->out_d, st));
+    } else if (op->p2.supported) {
+        CUDA_TRY(launch2d_cycle(op->p2, op->g, const_cast<double*>(x), nullptr, b, nullptr, 0, 0.0,
+                                1.0, op->partials, op->hist, op->out_i, op->out_d, st));
     } else {
         int rc = launch_cycle(op, x, nullptr, b, nullptr, 0, 0.0, 1.0, st);
         if (rc) return rc;
@@ -441,6 +451,10 @@ int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
         CUDA_TRY(tb_launch_cycle(op->tb, op->g, x, x_alt, b, omegas_dev, Meff,
                                  op->sweeps_per_pass, tol, baseline, op->partials, op->hist,
                                  op->out_i, op->out_d, st));
+        out->launches = 1;
+    } else if (op->p2.supported) {
+        CUDA_TRY(launch2d_cycle(op->p2, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,
+                                op->partials, op->hist, op->out_i, op->out_d, st));
         out->launches = 1;
     } else {
         const int rc = launch_cycle(op, x, x_alt, b, omegas_dev, Meff, tol, baseline, st);
@@ -493,6 +507,11 @@ int srj_sweep_planes(srj_op* op, const double* x, double* x_out, const double* b
     const Geom& g = op->g;
     if (g.fam == F3D && op->p3.supported) {
         CUDA_TRY(launch3d_sweep(op->p3, g, x, x_out, b, omega, (int)z_begin, (int)z_end,
+                                op->slot_part[slot], op->slot_counter + slot, partial_dev, st));
+        return SRJ_OK;
+    }
+    if (op->p2.supported) {
+        CUDA_TRY(launch2d_sweep(op->p2, g, x, x_out, b, omega, (int)z_begin, (int)z_end,
                                 op->slot_part[slot], op->slot_counter + slot, partial_dev, st));
         return SRJ_OK;
     }

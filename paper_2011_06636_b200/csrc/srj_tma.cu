@@ -46,6 +46,14 @@ cudaError_t encode_field_map(CUtensorMap* map, const double* base, int nx, int n
     return encode(map, base, 2, dims, strides, box);
 }
 
+cudaError_t encode_field_map_pitched(CUtensorMap* map, const double* base, int width, int rows,
+                                     int pitch, int box_x, int box_y) {
+    const cuuint64_t dims[2] = {(cuuint64_t)width, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)pitch * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)box_x, (cuuint32_t)box_y};
+    return encode(map, base, 2, dims, strides, box);
+}
+
 cudaError_t encode_volume_map(CUtensorMap* map, const double* base, int nx, int ny, int nz,
                               int box_x, int box_y) {
     const cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};

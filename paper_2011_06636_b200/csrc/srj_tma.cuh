@@ -76,6 +76,11 @@ bool tma_available();
 cudaError_t encode_field_map(CUtensorMap* map, const double* base, int nx, int ny, int box_x,
                              int box_y);
 
+// Host: 2D map over rows of `width` valid values stored with row pitch `pitch`
+// (doubles; pitch*8 must be a multiple of 16).
+cudaError_t encode_field_map_pitched(CUtensorMap* map, const double* base, int width, int rows,
+                                     int pitch, int box_x, int box_y);
+
 // Host: 3D fp64 map over nz planes of nx x ny (plane pitch nx*ny), box of
 // box_x x box_y x 1, zero fill out of bounds.
 cudaError_t encode_volume_map(CUtensorMap* map, const double* base, int nx, int ny, int nz,

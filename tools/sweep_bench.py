@@ -16,7 +16,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("cases")
     ap.add_argument("--level", type=int, default=20)
-    ap.add_argument("--spp", type=int, default=1)
+    ap.add_argument("--spp", type=int, default=0, help="sweeps per pass (0: operator default)")
     ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
     import numpy as np
@@ -31,7 +31,7 @@ def main():
         n = int(n)
         p = srj.baseline_problem(fam, n, seed=0, device=dev, rhs_on_device=(fam != "2d5var"))
         A = p.A
-        if a.spp > 1:
+        if a.spp > 0:
             A.set_sweeps_per_pass(a.spp)
         b = A.field(p.b)
         x = A.new_field()
