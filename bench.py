@@ -142,11 +142,8 @@ def traffic_from_profile(config):
 
 
 def kernel_name(family, info):
-    if family == "3d7":
-        return "srj::k_cycle3d (TMA plane ring)"
-    if info.get("tb_supported") and info.get("sweeps_per_pass", 1) > 1:
-        return "srj::k_tb2d_cycle (TMA temporal blocking)"
-    return "srj::k_cycle"
+    from paper_2011_06636_b200._lib import OpInfo
+    return OpInfo.KERNELS.get(info.get("cycle_kernel"), "unknown")
 
 
 def cpu_sample(family, n, seed, budget_s):

@@ -64,7 +64,8 @@ enum srj_family {
     SRJ_STENCIL_1D3 = 1,     /* 1D 3-point, (-1, 2, -1)*dx2                 */
     SRJ_STENCIL_2D5 = 2,     /* 2D 5-point, (-1,-1, 4,-1,-1)*dx2            */
     SRJ_STENCIL_3D7 = 3,     /* 3D 7-point, 6*dx2 diagonal, -dx2 neighbours  */
-    SRJ_STENCIL_2D5_VAR = 4  /* 2D 5-point, harmonic-mean face coefficients  */
+    SRJ_STENCIL_2D5_VAR = 4, /* 2D 5-point, harmonic-mean face coefficients  */
+    SRJ_CSR = 5              /* general canonical CSR matrix (sparse.SparseMatrix) */
 };
 
 /* Outcome of one cycle; mirrors the reference's CycleStats plus the buffer
@@ -87,6 +88,14 @@ typedef struct srj_op_desc {
      * face_y: ny+1 rows of nx faces (row j sits between rows j-1 and j). */
     const double* face_x;
     const double* face_y;
+    /* SRJ_CSR only (nx = n, ny = nz = 1; vectors carry no ghosts): canonical
+     * CSR -- ascending columns, duplicates summed, as sparse.SparseMatrix keeps
+     * it (sparse.py:28-44) -- and 1.0/diagonal, all device pointers. */
+    int64_t nnz;
+    const int64_t* row_ptr;
+    const int32_t* col_idx;
+    const double* values;
+    const double* inv_diag;
 } srj_op_desc;
 
 typedef struct srj_cycle_out {
@@ -123,7 +132,15 @@ typedef struct srj_op_info {
     int32_t tb_blocks;
     int32_t tb_occupancy;      /* resident CTAs per SM of the smallest TB variant */
     int32_t tb_tiles;
+    int32_t cycle_kernel;      /* enum srj_cycle_kernel serving srj_run_cycle now */
 } srj_op_info;
+
+enum srj_cycle_kernel {
+    SRJ_KERNEL_GENERIC = 0,    /* persistent row walker (any family)            */
+    SRJ_KERNEL_TB2D = 1,       /* temporally blocked 2D (sweeps_per_pass > 1)   */
+    SRJ_KERNEL_TILE2D = 2,     /* TMA tile streaming 2D (constant / variable)   */
+    SRJ_KERNEL_PLANE3D = 3     /* TMA plane streaming 3D                        */
+};
 int srj_op_describe(const srj_op* op, srj_op_info* info);
 
 /* sum_i (b - A x)_i^2 -> *sumsq_host.  Synchronises `stream`. */
@@ -142,6 +159,15 @@ int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
                   const double* omegas_dev, int32_t M, double tol, double baseline,
                   double res_before, int64_t budget, double* history_host,
                   srj_cycle_out* out, void* stream);
+
+/* Same cycle under the solution-difference infinity norm (solver.py:200-203,
+ * 224-228, 242-243): sweep k's norm is max|x_{k+1} - x_k| (bit-identical to
+ * numpy), tested before the next sweep; res_before = the incoming norm or NaN
+ * when unknown.  history_host receives the norm after each executed sweep. */
+int srj_run_cycle_diffinf(srj_op* op, double* x, double* x_alt, const double* b,
+                          const double* omegas_dev, int32_t M, double tol, double res_before,
+                          int64_t budget, double* history_host, srj_cycle_out* out,
+                          void* stream);
 
 /* x_out = x + omega * inv_diag * (b - A x)  (one weighted Jacobi sweep). */
 int srj_sweep(srj_op* op, const double* x, double* x_out, const double* b,

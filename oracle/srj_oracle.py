@@ -201,6 +201,26 @@ class StencilCPU:
         return y
 
 
+class CsrCPU:
+    """General CSR operator: scipy's csr_matvec is the reference's own SpMV
+    (solver.py:233 -> sparse.py:81), so the oracle calls it directly."""
+
+    def __init__(self, csr):
+        self.csr = csr
+        self.n = csr.shape[0]
+        self.inv_diag = 1.0 / csr.diagonal()
+
+    def residual(self, x, b):
+        r = b - self.csr.dot(x)
+        return r, float(np.dot(r, r))
+
+    def update(self, x, r, w):
+        return x + w * (self.inv_diag * r)
+
+    def matvec(self, x):
+        return self.csr.dot(x)
+
+
 def stencil(family, n, dx2=None, fx=None, fy=None):
     dims = {"1d3": (n, 1, 1), "2d5": (n, n, 1), "3d7": (n, n, n), "2d5var": (n, n, 1)}[family]
     if dx2 is None:
@@ -265,13 +285,40 @@ class Oracle:
                 history.append((total + executed, res_now))
         return x, r, res_now, executed, res_now <= tol
 
+    def cycle_diff(self, x, res_now, ordered, tol, budget, history, total):
+        """solver.py:200-203,216-249 with the solution-difference infinity norm;
+        returns (x, res_now, executed, res_before)."""
+        executed = 0
+        res_before = res_now
+        for w in ordered:
+            if res_now is not None and res_now <= tol:
+                break
+            if executed >= budget:
+                break
+            r, _ = self.op.residual(x, self.b)
+            x_new = self.op.update(x, r, w)
+            res_now = float(np.max(np.abs(x_new - x)))
+            x = x_new
+            executed += 1
+            if not math.isfinite(res_now) or not np.all(np.isfinite(x)):
+                raise OracleDiverged(executed, w)
+            if history is not None:
+                history.append((total + executed, res_now))
+            if res_before is None:
+                res_before = res_now
+        return x, res_now, executed, res_before
+
     def solve(self, x0, controller="heuristic", tol=1e-8, relative=True, max_iterations=10**9,
               max_cycles=None, fixed_M=None, record_history=True, t_hi=0.4, t_lo=0.2,
-              ordered=None):
+              ordered=None, diff=False):
         """controller: heuristic | increasing | fixed (fixed_M) | jacobi |
-        custom (a fixed ordered-omega tuple, e.g. a CJM scheme)."""
+        custom (a fixed ordered-omega tuple, e.g. a CJM scheme).  diff: the
+        solution-difference infinity norm (heuristic / jacobi controllers)."""
         t0 = time.perf_counter()
         x = np.ascontiguousarray(x0, dtype=np.float64).copy()
+        if diff:
+            return self._solve_diff(x, controller, tol, max_iterations, record_history, t_hi,
+                                    t_lo, t0)
         r, s = self.op.residual(x, self.b)
         baseline = 1.0
         if relative:
@@ -319,6 +366,43 @@ class Oracle:
                     level = next_level(ratio_prev, level, t_hi, t_lo)
             elif controller == "increasing":
                 level = min(level + 1, TOP)
+        return OracleReport(converged, total, cycles, x, history or [],
+                            time.perf_counter() - t0)
+
+    def _solve_diff(self, x, controller, tol, max_iterations, record_history, t_hi, t_lo, t0):
+        """solve() under the solution-difference norm (solver.py:289-331 with
+        baseline 1 and no initial residual)."""
+        history = [] if record_history else None
+        level, total, cycles, ratio_prev, res = 0, 0, [], None, None
+        converged = False
+        while True:
+            if controller == "jacobi":
+                seq, lvl, M = (1.0,), None, 1
+            else:
+                M = LADDER[level]
+                seq, lvl = scheme(M)
+            x, res_now, executed, before = self.cycle_diff(x, res, seq, tol,
+                                                           max_iterations - total, history,
+                                                           total)
+            after = res_now if res_now is not None else float("nan")
+            if before is None:
+                before = after
+            total += executed
+            if executed > 0:
+                ok = before > 0 and after > 0
+                cycles.append(CycleRecord(len(cycles), lvl if lvl is not None else -1, M,
+                                          executed, before, after,
+                                          avg_rate(before, after, executed) if ok else math.inf))
+                if ok:
+                    ratio_prev = after / before
+            res = res_now
+            if res is not None and res <= tol:
+                converged = True
+                break
+            if total >= max_iterations:
+                break
+            if controller == "heuristic" and ratio_prev is not None and math.isfinite(ratio_prev):
+                level = next_level(ratio_prev, level, t_hi, t_lo)
         return OracleReport(converged, total, cycles, x, history or [],
                             time.perf_counter() - t0)
 

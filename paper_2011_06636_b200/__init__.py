@@ -10,10 +10,14 @@ hand-written sm_100a kernels behind the C ABI in include/srj.h
 """
 
 from .chebyshev import amplification_eval, cheb_eval, cheb_roots, lambda_max, lambda_star
-from .operators import Field, StencilOperator, fill_uniform_rhs, relative_residual
+from .operators import (DeviceOperator, Field, StencilOperator, fill_uniform_rhs,
+                        relative_residual)
 from .problems import (ABSOLUTE_L2, CONFIGS, RELATIVE_L2, SOLUTION_DIFF_INF, ProblemInstance,
-                       baseline_problem, config_problem, diffusion_2d_varcoef, poisson_1d,
-                       poisson_2d, poisson_3d)
+                       baseline_problem, config_problem, diffusion_2d_varcoef,
+                       laplace_2d_neumann, poisson_1d, poisson_2d, poisson_3d,
+                       random_tridiagonal)
+from .sparse import (SparseMatrix, diff_inf, matvec, relative_residual_l2, residual_l2,
+                     weighted_jacobi_sweep)
 from .rng import SplitMix64, derive_seed, uniform_rhs
 from .schemes import (LEVEL_TABLE_M, MAX_LEVEL, ORDER_GRID_SIZE, SrjScheme,
                       generate_cjm_scheme, generate_srj_scheme, order_for_stability,

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libsrj.so")
 ABI_VERSION = 1
 
 SRJ_OK, SRJ_DIVERGED, SRJ_BAD_ARGUMENT, SRJ_CUDA_ERROR = 0, 1, 2, 3
-SRJ_STENCIL_1D3, SRJ_STENCIL_2D5, SRJ_STENCIL_3D7, SRJ_STENCIL_2D5_VAR = 1, 2, 3, 4
+SRJ_STENCIL_1D3, SRJ_STENCIL_2D5, SRJ_STENCIL_3D7, SRJ_STENCIL_2D5_VAR, SRJ_CSR = 1, 2, 3, 4, 5
 CYCLE_RAN, CYCLE_CONVERGED, CYCLE_DIVERGED = 0, 1, 2
 
 # Every symbol include/srj.h declares (checked by tests/test_abi.py).
@@ -26,7 +26,7 @@ EXPORTED_SYMBOLS = (
     "srj_op_layout", "srj_op_diag", "srj_op_set_sweeps_per_pass", "srj_op_describe",
     "srj_residual_sq",
     "srj_run_cycle", "srj_sweep", "srj_matvec", "srj_fill_uniform_rhs",
-    "srj_op_planes", "srj_sweep_planes",
+    "srj_op_planes", "srj_sweep_planes", "srj_run_cycle_diffinf",
 )
 
 
@@ -36,6 +36,8 @@ class OpDesc(ctypes.Structure):
         ("nx", c_int64), ("ny", c_int64), ("nz", c_int64),
         ("dx2", c_double),
         ("face_x", c_void_p), ("face_y", c_void_p),
+        ("nnz", c_int64), ("row_ptr", c_void_p), ("col_idx", c_void_p),
+        ("values", c_void_p), ("inv_diag", c_void_p),
     ]
 
 
@@ -49,7 +51,12 @@ class CycleOut(ctypes.Structure):
 class OpInfo(ctypes.Structure):
     _fields_ = [(name, c_int32) for name in (
         "num_sms", "cycle_blocks", "cycle_threads", "sweeps_per_pass", "tb_supported",
-        "tb_blocks", "tb_occupancy", "tb_tiles")]
+        "tb_blocks", "tb_occupancy", "tb_tiles", "cycle_kernel")]
+
+    KERNELS = {0: "srj::k_cycle (generic row walker)",
+               1: "srj::k_tb2d_cycle (TMA temporal blocking)",
+               2: "srj::k_cycle2d (TMA tile streaming)",
+               3: "srj::k_cycle3d (TMA plane ring)"}
 
     def as_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
@@ -79,6 +86,9 @@ def _declare(L):
     L.srj_matvec.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p]
     L.srj_fill_uniform_rhs.argtypes = [c_void_p, c_int64, c_uint64, c_int64, c_int32, c_void_p]
     L.srj_op_planes.argtypes = [c_void_p]
+    L.srj_run_cycle_diffinf.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                        c_int32, c_double, c_double, c_int64, c_void_p,
+                                        POINTER(CycleOut), c_void_p]
     L.srj_sweep_planes.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int64,
                                    c_int64, c_void_p, c_int32, c_void_p]
     for name in EXPORTED_SYMBOLS:

@@ -53,7 +53,41 @@ struct CycleArgs {
     double* hist;          // [M+1] relative residual of x_k
     int* out_i;            // executed, status
     double* out_d;         // final sum of squares, res_after
+    int diff;              // 1: solution-difference infinity norm (no baseline, no lag)
 };
+
+// Solution-difference norm cycle (reference solver.py:200-203,224-228,242-243):
+// sweep k produces x_{k+1} and d_k = max|x_{k+1} - x_k| (a max: bit-identical
+// to numpy in any order); the test before sweep k+1 uses d_k, so there is no
+// lag and no residual tail.
+template <int FAM>
+__device__ __forceinline__ void cycle_diff(const CycleArgs& a, int u0, int u1, double* sh) {
+    const int nb = gridDim.x;
+    double* const buf[2] = {const_cast<double*>(a.xa), a.xb};
+    int executed = a.M, status = kStatusRan;
+    double res = 0.0;
+    for (int k = 0; k < a.M; ++k) {
+        double d = walk_units<FAM, kSweepDiff>(a.g, buf[k & 1], buf[(k + 1) & 1], a.b,
+                                               a.omegas[k], u0, u1);
+        double* part = a.partials + (k & 1) * nb;
+        d = block_allmax(d, sh);
+        if (threadIdx.x == 0) part[blockIdx.x] = d;
+        grid_barrier();
+        double m = 0.0;
+        for (int q = threadIdx.x; q < nb; q += blockDim.x) m = nanmax(m, __ldcg(part + q));
+        res = block_allmax(m, sh);
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.hist[k + 1] = res;
+        if (!isfinite(res)) { executed = k + 1; status = kStatusDiverged; break; }
+        if (res <= a.tol) { executed = k + 1; status = kStatusConverged; break; }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.out_i[0] = executed;
+        a.out_i[1] = status;
+        a.out_i[2] = executed & 1;
+        a.out_d[0] = res;
+        a.out_d[1] = res;
+    }
+}
 
 template <int FAM>
 __global__ void __launch_bounds__(1024) k_cycle(CycleArgs a) {
@@ -61,6 +95,10 @@ __global__ void __launch_bounds__(1024) k_cycle(CycleArgs a) {
     const int nb = gridDim.x;
     const int u0 = (int)((long long)a.g.units * blockIdx.x / nb);
     const int u1 = (int)((long long)a.g.units * (blockIdx.x + 1) / nb);
+    if (a.diff) {
+        cycle_diff<FAM>(a, u0, u1, sh);
+        return;
+    }
     double* const buf[2] = {const_cast<double*>(a.xa), a.xb};
     int executed = a.M, status = kStatusRan;
     double S = 0.0, res = 0.0;
@@ -197,6 +235,7 @@ static const void* cycle_kernel_for(int fam) {
         case F1D: return cycle_kernel<F1D>();
         case F2D: return cycle_kernel<F2D>();
         case F3D: return cycle_kernel<F3D>();
+        case FCSR: return cycle_kernel<FCSR>();
         default: return cycle_kernel<F2DV>();
     }
 }
@@ -209,6 +248,7 @@ static int launch_apply(srj_op* op, const double* x, double* out, const double* 
         case F1D: k_apply<F1D, MODE><<<blocks, kThreads, 0, st>>>(op->g, x, out, b, w); break;
         case F2D: k_apply<F2D, MODE><<<blocks, kThreads, 0, st>>>(op->g, x, out, b, w); break;
         case F3D: k_apply<F3D, MODE><<<blocks, kThreads, 0, st>>>(op->g, x, out, b, w); break;
+        case FCSR: k_apply<FCSR, MODE><<<blocks, kThreads, 0, st>>>(op->g, x, out, b, w); break;
         default: k_apply<F2DV, MODE><<<blocks, kThreads, 0, st>>>(op->g, x, out, b, w); break;
     }
     CUDA_TRY(cudaGetLastError());
@@ -224,14 +264,18 @@ const char* srj_last_error(void) { return g_last_error.c_str(); }
 int srj_op_create(const srj_op_desc* d, srj_op** out) {
     if (!d || !out) return fail(SRJ_BAD_ARGUMENT, "null argument");
     *out = nullptr;
-    if (d->family < SRJ_STENCIL_1D3 || d->family > SRJ_STENCIL_2D5_VAR)
+    if (d->family < SRJ_STENCIL_1D3 || d->family > SRJ_CSR)
         return fail(SRJ_BAD_ARGUMENT, "unknown stencil family");
     if (d->nx < 1 || d->ny < 1 || d->nz < 1)
         return fail(SRJ_BAD_ARGUMENT, "extents must be positive");
     const bool var = d->family == SRJ_STENCIL_2D5_VAR;
+    const bool csr = d->family == SRJ_CSR;
     if (var && (!d->face_x || !d->face_y))
         return fail(SRJ_BAD_ARGUMENT, "variable-coefficient operator needs face_x and face_y");
-    if (!var && !(d->dx2 > 0.0))
+    if (csr && (!d->row_ptr || !d->col_idx || !d->values || !d->inv_diag || d->ny != 1 ||
+                d->nz != 1 || d->nnz < 1))
+        return fail(SRJ_BAD_ARGUMENT, "CSR operator needs row_ptr, col_idx, values, inv_diag, nnz and ny == nz == 1");
+    if (!var && !csr && !(d->dx2 > 0.0))
         return fail(SRJ_BAD_ARGUMENT, "dx2 must be positive");
     if (d->family == SRJ_STENCIL_1D3 && (d->ny != 1 || d->nz != 1))
         return fail(SRJ_BAD_ARGUMENT, "1D operator needs ny == nz == 1");
@@ -252,7 +296,9 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
     g.ny = (int)d->ny;
     g.nz = (int)d->nz;
     g.n = d->nx * d->ny * d->nz;
-    g.plane = d->family == SRJ_STENCIL_1D3 ? 1 : (d->family == SRJ_STENCIL_3D7 ? d->nx * d->ny : d->nx);
+    g.plane = csr ? 0
+                  : d->family == SRJ_STENCIL_1D3 ? 1
+                  : (d->family == SRJ_STENCIL_3D7 ? d->nx * d->ny : d->nx);
     g.rows = (int)rows;
     g.upr = (int)upr;
     g.units = (int)(rows * upr);
@@ -262,6 +308,10 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
     g.inv_diag = 1.0 / g.c_diag;              // sparse.py:44
     g.fx = d->face_x;
     g.fy = d->face_y;
+    g.rp = reinterpret_cast<const long long*>(d->row_ptr);
+    g.ci = d->col_idx;
+    g.cv = d->values;
+    g.cinv = d->inv_diag;
 
     cudaDeviceProp prop;
     cudaError_t e = cudaGetDeviceProperties(&prop, d->device);
@@ -353,7 +403,8 @@ int srj_op_layout(const srj_op* op, int64_t* n, int64_t* halo) {
 
 int srj_op_diag(const srj_op* op, double* diag, double* inv_diag) {
     if (!op) return fail(SRJ_BAD_ARGUMENT, "null operator");
-    if (op->g.fam == F2DV) return fail(SRJ_BAD_ARGUMENT, "variable-coefficient diagonal is per point");
+    if (op->g.fam == F2DV || op->g.fam == FCSR)
+        return fail(SRJ_BAD_ARGUMENT, "this operator's diagonal is per point");
     if (diag) *diag = op->g.c_diag;
     if (inv_diag) *inv_diag = op->g.inv_diag;
     return SRJ_OK;
@@ -369,6 +420,10 @@ int srj_op_describe(const srj_op* op, srj_op_info* info) {
     info->tb_blocks = op->tb.blocks[op->tb.small_variant];
     info->tb_occupancy = op->tb.occupancy;
     info->tb_tiles = op->tb.ntiles[op->tb.small_variant];
+    info->cycle_kernel = op->p3.supported                                 ? SRJ_KERNEL_PLANE3D
+                         : (op->sweeps_per_pass > 1 && op->tb.supported) ? SRJ_KERNEL_TB2D
+                         : op->p2.supported                               ? SRJ_KERNEL_TILE2D
+                                                                          : SRJ_KERNEL_GENERIC;
     return SRJ_OK;
 }
 
@@ -381,8 +436,9 @@ int srj_op_set_sweeps_per_pass(srj_op* op, int32_t s) {
 
 static int launch_cycle(srj_op* op, const double* xa, double* xb, const double* b,
                         const double* omegas, int M, double tol, double baseline,
-                        cudaStream_t st) {
+                        cudaStream_t st, int diff = 0) {
     CycleArgs a;
+    a.diff = diff;
     a.g = op->g;
     a.xa = xa;
     a.xb = xb;
@@ -477,6 +533,44 @@ int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
     return SRJ_OK;
 }
 
+int srj_run_cycle_diffinf(srj_op* op, double* x, double* x_alt, const double* b,
+                          const double* omegas_dev, int32_t M, double tol, double res_before,
+                          int64_t budget, double* history_host, srj_cycle_out* out,
+                          void* stream) {
+    if (!op || !x || !x_alt || !b || !out) return fail(SRJ_BAD_ARGUMENT, "null argument");
+    if (M < 1 || M > kMaxSchemeLength) return fail(SRJ_BAD_ARGUMENT, "scheme length out of range");
+    if (!omegas_dev) return fail(SRJ_BAD_ARGUMENT, "null omegas");
+    DeviceGuard guard(op->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    std::memset(out, 0, sizeof(*out));
+    out->res_before = res_before;
+    out->res_after = res_before;
+    // the incoming difference norm, when known (a NaN means unknown), is tested
+    // before the first sweep (solver.py:217-220)
+    if (res_before == res_before && res_before <= tol) {
+        out->status = SRJ_CYCLE_CONVERGED;
+        return SRJ_OK;
+    }
+    const int Meff = (int)std::min<int64_t>(M, std::max<int64_t>(budget, 0));
+    if (Meff == 0) return SRJ_OK;
+    const int rc = launch_cycle(op, x, x_alt, b, omegas_dev, Meff, tol, 1.0, st, /*diff=*/1);
+    if (rc) return rc;
+    out->launches = 1;
+    CUDA_TRY(cudaMemcpyAsync(op->h_out_i, op->out_i, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(op->h_out_d, op->out_d, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (history_host)
+        CUDA_TRY(cudaMemcpyAsync(op->h_hist, op->hist, (Meff + 1) * sizeof(double),
+                                 cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    out->executed = op->h_out_i[0];
+    out->status = op->h_out_i[1];
+    out->result_in_alt = op->h_out_i[2];
+    out->res_after = op->h_out_d[1];
+    if (history_host && out->executed > 0)
+        std::memcpy(history_host, op->h_hist + 1, out->executed * sizeof(double));
+    return SRJ_OK;
+}
+
 int srj_sweep(srj_op* op, const double* x, double* x_out, const double* b, double omega, void* stream) {
     if (!op || !x || !x_out || !b) return fail(SRJ_BAD_ARGUMENT, "null argument");
     DeviceGuard guard(op->device);
@@ -491,7 +585,7 @@ int srj_matvec(srj_op* op, const double* x, double* y, void* stream) {
 
 int64_t srj_op_planes(const srj_op* op) {
     if (!op) return -1;
-    return op->g.fam == F3D ? op->g.nz : (op->g.fam == F1D ? 1 : op->g.ny);
+    return op->g.fam == F3D ? op->g.nz : ((op->g.fam == F1D || op->g.fam == FCSR) ? 1 : op->g.ny);
 }
 
 int srj_sweep_planes(srj_op* op, const double* x, double* x_out, const double* b, double omega,
@@ -534,6 +628,7 @@ int srj_sweep_planes(srj_op* op, const double* x, double* x_out, const double* b
         case F1D: SRJ_RANGE(F1D) break;
         case F2D: SRJ_RANGE(F2D) break;
         case F3D: SRJ_RANGE(F3D) break;
+        case FCSR: SRJ_RANGE(FCSR) break;
         default: SRJ_RANGE(F2DV) break;
     }
 #undef SRJ_RANGE

@@ -14,7 +14,7 @@
 
 namespace srj {
 
-enum Family { F1D = 1, F2D = 2, F3D = 3, F2DV = 4 };
+enum Family { F1D = 1, F2D = 2, F3D = 3, F2DV = 4, FCSR = 5 };
 
 // Cycle outcome codes (match enum srj_cycle_status in include/srj.h).
 constexpr int kStatusRan = 0;
@@ -37,7 +37,35 @@ struct Geom {
     double inv_diag;    // 1.0 / c_diag
     const double* fx;   // var-coef faces (see srj.h)
     const double* fy;
+    // general CSR operator (canonical: sorted columns, no duplicates)
+    const long long* rp;  // row pointers [n+1]
+    const int* ci;        // column indices [nnz]
+    const double* cv;     // values [nnz]
+    const double* cinv;   // 1.0 / diagonal [n]
 };
+
+// max that propagates NaN (fmax would drop it): a NaN difference must read
+// as non-finite in the solution-difference norm.
+__device__ __forceinline__ double nanmax(double a, double b) {
+    return (a != a || b != b) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(a, b);
+}
+
+__device__ __forceinline__ double warp_allmax(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = nanmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ double block_allmax(double v, double* sh) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+    v = warp_allmax(v);
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double t = lane < nw ? sh[lane] : 0.0;
+    return warp_allmax(t);
+}
 
 __device__ __forceinline__ double warp_allsum(double v) {
     // xor butterfly: partners add the same two operands (commutative), so

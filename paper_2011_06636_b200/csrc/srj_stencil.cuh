@@ -57,6 +57,13 @@ __device__ __forceinline__ double apply_at(const Geom& g, const double* x,
         y = DADD(y, DMUL(c, xe));
         y = DADD(y, DMUL(c, xn));
         y = DADD(y, DMUL(c, x[k + pl]));
+    } else if constexpr (FAM == FCSR) {
+        // scipy csr_matvec (sparsetools): sum starts at 0, ascending columns
+        const long long e = g.rp[k + 1];
+        y = 0.0;
+        for (long long jj = g.rp[k]; jj < e; ++jj) y = DADD(y, DMUL(__ldg(g.cv + jj), x[__ldg(g.ci + jj)]));
+        xc = x[k];
+        inv = __ldg(g.cinv + k);
     } else {  // F2DV: faces pre-scaled by dx2; CSR stores -face off the diagonal
         const long long nx = g.nx;
         const long long row = j;

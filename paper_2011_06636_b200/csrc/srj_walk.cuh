@@ -10,7 +10,9 @@
 
 namespace srj {
 
-enum Mode { kSweep = 0, kResid = 1, kMatvec = 2 };
+// kSweepDiff: sweep returning max |x' - x| (solution-difference norm,
+// reference solver.py:224-228) instead of sum r^2.
+enum Mode { kSweep = 0, kResid = 1, kMatvec = 2, kSweepDiff = 3 };
 
 // Walk the 32-point x-row units [u0, u1) of the grid.  Warps take units
 // round-robin so a CTA streams through consecutive rows together (coalesced
@@ -33,6 +35,11 @@ __device__ __forceinline__ double walk_units(const Geom& g, const double* __rest
             const double y = apply_at<FAM>(g, x, k, i, j, xc, inv);
             if constexpr (MODE == kMatvec) {
                 out[k] = y;
+            } else if constexpr (MODE == kSweepDiff) {
+                const double r = DSUB(__ldg(b + k), y);
+                const double xn = relax(xc, inv, r, w);
+                out[k] = xn;
+                acc = nanmax(acc, fabs(DSUB(xn, xc)));
             } else {
                 const double r = DSUB(__ldg(b + k), y);
                 acc = fma(r, r, acc);

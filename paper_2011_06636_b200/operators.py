@@ -1,15 +1,19 @@
-"""Device-resident structured operators: the drop-in for `sparse.SparseMatrix`
-on the solve path.
+"""Device-resident operators: the drop-in for `sparse.SparseMatrix` on the
+solve path.
 
 The reference's `run_cycle` touches only `A.inv_diag` and `A.scipy_csr().dot`
 (reference solver.py:192-193,209,225,233); `ProblemInstance` checks `A.n`
-(problems.py:37-39).  A `StencilOperator` exposes the same surface (`n`,
-`diag`, `inv_diag`, `scipy_csr()` for interop) but never stores a matrix on
-the device: the sm_100a kernels recompute the constant-coefficient stencil, or
-read two face-coefficient streams, in the exact CSR column order.
+(problems.py:37-39).  Every operator here exposes that surface (`n`, `diag`,
+`inv_diag`, `scipy_csr()` for interop) and runs its sweeps in libsrj:
 
-Device vectors are `Field`s: n interior fp64 values with one ghost plane
-(`halo` elements) before and after, zero for a Dirichlet side.  Every C-ABI
+* `StencilOperator` -- structured Dirichlet stencils; the sm_100a kernels
+  recompute the constant-coefficient stencil, or read two face-coefficient
+  streams, in the exact CSR column order; no matrix is stored.
+* `sparse.SparseMatrix` -- any canonical CSR matrix (unstructured problems,
+  Neumann grids, random tridiagonals), swept by the generic CSR kernel.
+
+Device vectors are `Field`s: n interior fp64 values with `halo` ghost elements
+before and after (one grid plane for stencils, zero for CSR).  Every C-ABI
 pointer addresses the first interior element.
 """
 
@@ -42,7 +46,7 @@ def _stream_handle(device):
 
 
 class Field:
-    """n interior fp64 values in a device buffer with `halo` ghosts per side."""
+    """n interior fp64 values in a buffer with `halo` ghosts per side."""
 
     def __init__(self, n: int, halo: int, device, buf=None):
         torch = _torch()
@@ -74,120 +78,19 @@ class Field:
         return Field(self.n, self.halo, self.device, self.buf.clone())
 
 
-@dataclass(frozen=True)
-class Grid:
-    family: str
-    nx: int
-    ny: int = 1
-    nz: int = 1
+class DeviceOperator:
+    """Device plumbing shared by every operator: handle, Fields, sweeps,
+    residuals and the per-cycle C-ABI calls.  Subclasses set `n`, `halo`,
+    `_device` and implement `_fill_desc`."""
 
-    @property
-    def n(self) -> int:
-        return self.nx * self.ny * self.nz
+    n: int
+    halo: int
 
-    @property
-    def halo(self) -> int:
-        return {"1d3": 1, "2d5": self.nx, "2d5var": self.nx, "3d7": self.nx * self.ny}[self.family]
-
-
-class StencilOperator:
-    """Symmetric Dirichlet stencil operator on a structured grid.
-
-    Constant coefficient ("1d3", "2d5", "3d7"): off-diagonals -dx2 and diagonal
-    2d*dx2 with dx2 = (N+1)^2, as `poisson_1d` / `poisson_3d` assemble them
-    (reference problems.py:50-69,148-177).  Variable coefficient ("2d5var"):
-    `face_x` (ny, nx+1) and `face_y` (ny+1, nx) hold the dx2-scaled
-    harmonic-mean face coefficients; off-diagonals are -face and the diagonal is
-    ((c_w + c_e) + c_s) + c_n.
-    """
-
-    def __init__(self, family: str, shape, dx2: float | None = None,
-                 face_x=None, face_y=None, device=None):
-        if family not in FAMILIES:
-            raise ValueError(f"unknown stencil family {family!r}")
-        dims = tuple(int(v) for v in (shape if isinstance(shape, (tuple, list)) else (shape,)))
-        want = {"1d3": 1, "2d5": 2, "2d5var": 2, "3d7": 3}[family]
-        if len(dims) != want or min(dims) < 1:
-            raise ValueError(f"{family} needs {want} positive extents, got {shape!r}")
-        self.family = family
-        self.shape = dims
-        self.grid = Grid(family, *dims)
-        self.n = self.grid.n
-        self.halo = self.grid.halo
+    def _init_device(self, device) -> None:
         self._device = device
-        if family == "2d5var":
-            if face_x is None or face_y is None:
-                raise ValueError("variable-coefficient operator needs face_x and face_y")
-            nx, ny = dims
-            fx = np.asarray(face_x, dtype=np.float64) if isinstance(face_x, np.ndarray) else face_x
-            fy = np.asarray(face_y, dtype=np.float64) if isinstance(face_y, np.ndarray) else face_y
-            if tuple(fx.shape) != (ny, nx + 1) or tuple(fy.shape) != (ny + 1, nx):
-                raise ValueError("face arrays must be (ny, nx+1) and (ny+1, nx)")
-            self.face_x, self.face_y = fx, fy
-            self.dx2 = None
-        else:
-            if dx2 is None:
-                dx2 = (dims[0] + 1.0) ** 2
-            if not dx2 > 0.0:
-                raise ValueError("dx2 must be positive")
-            self.dx2 = float(dx2)
-            self.face_x = self.face_y = None
         self._handle = None
-        self._dev_faces = None
-        self._diag = None
+        self._keep = ()  # device arrays the native handle points into
 
-    # ------------------------------------------------------------ SparseMatrix surface
-    @property
-    def diag_value(self) -> float:
-        d = {"1d3": 2.0, "2d5": 4.0, "3d7": 6.0}[self.family]
-        return d * self.dx2
-
-    @property
-    def diag(self) -> np.ndarray:
-        if self._diag is None:
-            if self.family == "2d5var":
-                fx = _as_numpy(self.face_x)
-                fy = _as_numpy(self.face_y)
-                self._diag = (((fx[:, :-1] + fx[:, 1:]) + fy[:-1, :]) + fy[1:, :]).reshape(-1)
-            else:
-                self._diag = np.full(self.n, self.diag_value)
-        return self._diag
-
-    @property
-    def inv_diag(self) -> np.ndarray:
-        return 1.0 / self.diag
-
-    def scipy_csr(self):
-        """Host CSR with the reference's canonical layout (interop and tests)."""
-        import scipy.sparse
-        rows, cols, vals = self.coo()
-        return scipy.sparse.csr_matrix((vals, (rows, cols)), shape=(self.n, self.n))
-
-    def coo(self):
-        g = self.grid
-        ids = np.arange(self.n).reshape(g.nz, g.ny, g.nx)
-        diag = self.diag
-        rows, cols, vals = [ids.reshape(-1)], [ids.reshape(-1)], [diag]
-        if self.family == "2d5var":
-            fx = _as_numpy(self.face_x)
-            fy = _as_numpy(self.face_y)
-            inner_x = fx[:, 1:-1]          # faces between i and i+1
-            inner_y = fy[1:-1, :]          # faces between j and j+1
-            a = ids[0, :, :-1].reshape(-1); b = ids[0, :, 1:].reshape(-1)
-            rows += [a, b]; cols += [b, a]; vals += [-inner_x.reshape(-1)] * 2
-            a = ids[0, :-1, :].reshape(-1); b = ids[0, 1:, :].reshape(-1)
-            rows += [a, b]; cols += [b, a]; vals += [-inner_y.reshape(-1)] * 2
-        else:
-            off = -1.0 * self.dx2
-            for axis in (2, 1, 0):
-                if ids.shape[axis] < 2:
-                    continue
-                lo = np.take(ids, np.arange(ids.shape[axis] - 1), axis=axis).reshape(-1)
-                hi = np.take(ids, np.arange(1, ids.shape[axis]), axis=axis).reshape(-1)
-                rows += [lo, hi]; cols += [hi, lo]; vals += [np.full(lo.size, off)] * 2
-        return np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
-
-    # ------------------------------------------------------------ device side
     @property
     def device(self):
         torch = _torch()
@@ -201,23 +104,18 @@ class StencilOperator:
             self._handle = self._create()
         return self._handle
 
+    def _fill_desc(self, desc, dev) -> None:
+        raise NotImplementedError
+
     def _create(self):
         torch = _torch()
         L = _lib.lib()
         if not torch.cuda.is_available():
             raise _lib.SrjLibraryError("the SRJ device path needs a CUDA device (no CPU fallback)")
         dev = self.device
-        g = self.grid
         desc = _lib.OpDesc()
-        desc.family = FAMILIES[self.family]
         desc.device = dev.index if dev.index is not None else torch.cuda.current_device()
-        desc.nx, desc.ny, desc.nz = g.nx, g.ny, g.nz
-        desc.dx2 = self.dx2 if self.dx2 is not None else 0.0
-        if self.family == "2d5var":
-            fx = _to_device(self.face_x, dev).contiguous()
-            fy = _to_device(self.face_y, dev).contiguous()
-            self._dev_faces = (fx, fy)
-            desc.face_x, desc.face_y = fx.data_ptr(), fy.data_ptr()
+        self._fill_desc(desc, dev)
         h = ctypes.c_void_p()
         _lib.check(L.srj_op_create(ctypes.byref(desc), ctypes.byref(h)), "srj_op_create")
         return h
@@ -265,12 +163,6 @@ class StencilOperator:
             int(z_begin), int(z_end), ctypes.c_void_p(partial_ptr), int(slot),
             _stream_handle(self.device)), "srj_sweep_planes")
 
-    @property
-    def planes(self) -> int:
-        """Planes along the slab axis (z in 3D, rows in 2D, 1 in 1D)."""
-        return {"1d3": 1, "2d5": self.shape[1], "2d5var": self.shape[1],
-                "3d7": self.shape[2]}[self.family]
-
     def matvec(self, x: Field):
         torch = _torch()
         y = torch.empty(self.n, dtype=torch.float64, device=self.device)
@@ -288,6 +180,18 @@ class StencilOperator:
             _stream_handle(self.device)), "srj_run_cycle")
         return out
 
+    def run_cycle_diffinf(self, x: Field, x_alt: Field, b: Field, omegas_dev, M: int,
+                          tol: float, res_before: float | None, budget: int,
+                          history: np.ndarray | None):
+        out = _lib.CycleOut()
+        hist_ptr = history.ctypes.data if history is not None else None
+        rb = float("nan") if res_before is None else float(res_before)
+        _lib.check(_lib.lib().srj_run_cycle_diffinf(
+            self.handle, x.ptr, x_alt.ptr, b.ptr, omegas_dev.data_ptr(), int(M), float(tol),
+            rb, int(budget), hist_ptr, ctypes.byref(out), _stream_handle(self.device)),
+            "srj_run_cycle_diffinf")
+        return out
+
     def __del__(self):
         h = getattr(self, "_handle", None)
         if h is not None and _lib._lib is not None:
@@ -295,6 +199,140 @@ class StencilOperator:
                 _lib._lib.srj_op_destroy(h)
             except Exception:
                 pass
+
+
+@dataclass(frozen=True)
+class Grid:
+    family: str
+    nx: int
+    ny: int = 1
+    nz: int = 1
+
+    @property
+    def n(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    @property
+    def halo(self) -> int:
+        return {"1d3": 1, "2d5": self.nx, "2d5var": self.nx, "3d7": self.nx * self.ny}[self.family]
+
+
+class StencilOperator(DeviceOperator):
+    """Symmetric Dirichlet stencil operator on a structured grid.
+
+    Constant coefficient ("1d3", "2d5", "3d7"): off-diagonals -dx2 and diagonal
+    2d*dx2 with dx2 = (N+1)^2, as `poisson_1d` / `poisson_3d` assemble them
+    (reference problems.py:50-69,148-177).  Variable coefficient ("2d5var"):
+    `face_x` (ny, nx+1) and `face_y` (ny+1, nx) hold the dx2-scaled
+    harmonic-mean face coefficients; off-diagonals are -face and the diagonal is
+    ((c_w + c_e) + c_s) + c_n.  Face arrays are captured when the native handle
+    is created.
+    """
+
+    def __init__(self, family: str, shape, dx2: float | None = None,
+                 face_x=None, face_y=None, device=None):
+        if family not in FAMILIES:
+            raise ValueError(f"unknown stencil family {family!r}")
+        dims = tuple(int(v) for v in (shape if isinstance(shape, (tuple, list)) else (shape,)))
+        want = {"1d3": 1, "2d5": 2, "2d5var": 2, "3d7": 3}[family]
+        if len(dims) != want or min(dims) < 1:
+            raise ValueError(f"{family} needs {want} positive extents, got {shape!r}")
+        self.family = family
+        self.shape = dims
+        self.grid = Grid(family, *dims)
+        self.n = self.grid.n
+        self.halo = self.grid.halo
+        self._init_device(device)
+        if family == "2d5var":
+            if face_x is None or face_y is None:
+                raise ValueError("variable-coefficient operator needs face_x and face_y")
+            nx, ny = dims
+            fx = np.asarray(face_x, dtype=np.float64) if isinstance(face_x, np.ndarray) else face_x
+            fy = np.asarray(face_y, dtype=np.float64) if isinstance(face_y, np.ndarray) else face_y
+            if tuple(fx.shape) != (ny, nx + 1) or tuple(fy.shape) != (ny + 1, nx):
+                raise ValueError("face arrays must be (ny, nx+1) and (ny+1, nx)")
+            self.face_x, self.face_y = fx, fy
+            self.dx2 = None
+        else:
+            if dx2 is None:
+                dx2 = (dims[0] + 1.0) ** 2
+            if not dx2 > 0.0:
+                raise ValueError("dx2 must be positive")
+            self.dx2 = float(dx2)
+            self.face_x = self.face_y = None
+        self._diag = None
+
+    # ------------------------------------------------------------ SparseMatrix surface
+    @property
+    def diag_value(self) -> float:
+        d = {"1d3": 2.0, "2d5": 4.0, "3d7": 6.0}[self.family]
+        return d * self.dx2
+
+    @property
+    def diag(self) -> np.ndarray:
+        if self._diag is None:
+            if self.family == "2d5var":
+                fx = _as_numpy(self.face_x)
+                fy = _as_numpy(self.face_y)
+                self._diag = (((fx[:, :-1] + fx[:, 1:]) + fy[:-1, :]) + fy[1:, :]).reshape(-1)
+            else:
+                self._diag = np.full(self.n, self.diag_value)
+        return self._diag
+
+    @property
+    def inv_diag(self) -> np.ndarray:
+        return 1.0 / self.diag
+
+    def scipy_csr(self):
+        """Host CSR with the reference's canonical layout (interop and tests)."""
+        import scipy.sparse
+        rows, cols, vals = self.coo()
+        m = scipy.sparse.csr_matrix((vals, (rows, cols)), shape=(self.n, self.n))
+        m.sum_duplicates()
+        m.sort_indices()
+        return m
+
+    def coo(self):
+        g = self.grid
+        ids = np.arange(self.n).reshape(g.nz, g.ny, g.nx)
+        diag = self.diag
+        rows, cols, vals = [ids.reshape(-1)], [ids.reshape(-1)], [diag]
+        if self.family == "2d5var":
+            fx = _as_numpy(self.face_x)
+            fy = _as_numpy(self.face_y)
+            inner_x = fx[:, 1:-1]          # faces between i and i+1
+            inner_y = fy[1:-1, :]          # faces between j and j+1
+            a = ids[0, :, :-1].reshape(-1); b = ids[0, :, 1:].reshape(-1)
+            rows += [a, b]; cols += [b, a]; vals += [-inner_x.reshape(-1)] * 2
+            a = ids[0, :-1, :].reshape(-1); b = ids[0, 1:, :].reshape(-1)
+            rows += [a, b]; cols += [b, a]; vals += [-inner_y.reshape(-1)] * 2
+        else:
+            off = -1.0 * self.dx2
+            for axis in (2, 1, 0):
+                if ids.shape[axis] < 2:
+                    continue
+                lo = np.take(ids, np.arange(ids.shape[axis] - 1), axis=axis).reshape(-1)
+                hi = np.take(ids, np.arange(1, ids.shape[axis]), axis=axis).reshape(-1)
+                rows += [lo, hi]; cols += [hi, lo]; vals += [np.full(lo.size, off)] * 2
+        return np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
+
+    @property
+    def planes(self) -> int:
+        """Planes along the slab axis (z in 3D, rows in 2D, 1 in 1D)."""
+        return {"1d3": 1, "2d5": self.shape[1], "2d5var": self.shape[1],
+                "3d7": self.shape[2]}[self.family]
+
+    # ------------------------------------------------------------ device side
+    def _fill_desc(self, desc, dev) -> None:
+        g = self.grid
+        desc.family = FAMILIES[self.family]
+        desc.nx, desc.ny, desc.nz = g.nx, g.ny, g.nz
+        desc.dx2 = self.dx2 if self.dx2 is not None else 0.0
+        if self.family == "2d5var":
+            fx = _to_device(self.face_x, dev).contiguous()
+            fy = _to_device(self.face_y, dev).contiguous()
+            self._keep = (fx, fy)
+            desc.face_x, desc.face_y = fx.data_ptr(), fy.data_ptr()
 
 
 def _as_numpy(a) -> np.ndarray:
@@ -326,7 +364,7 @@ def fill_uniform_rhs(field_or_tensor, seed: int, start: int = 0) -> None:
         _stream_handle(dev)), "srj_fill_uniform_rhs")
 
 
-def relative_residual(op: StencilOperator, x: Field, b: Field, x0: Field) -> float:
+def relative_residual(op: DeviceOperator, x: Field, b: Field, x0: Field) -> float:
     r0 = math.sqrt(op.residual_sq(x0, b))
     if r0 == 0.0:
         raise ValueError("initial residual is zero; relative residual undefined")

@@ -87,6 +87,67 @@ def poisson_3d(n: int, device=None) -> ProblemInstance:
 
 
 # ---------------------------------------------------------------------------
+# General-CSR problems: device SparseMatrix operators
+# ---------------------------------------------------------------------------
+
+def random_tridiagonal(N: int, seed: int, device=None) -> ProblemInstance:
+    """Random symmetric weakly diagonally dominant tridiagonal system
+    (reference problems.py:72-98): off-diagonals then diagonals drawn from one
+    SplitMix64 stream, non-dominant diagonals raised to the neighbour sum, the
+    end diagonals set to twice their single neighbour."""
+    from .sparse import SparseMatrix
+    if N < 2:
+        raise ValueError("N must be at least 2")
+    u = uniforms_counter(seed, 2 * N - 1)
+    off, diag = u[:N - 1], u[N - 1:]
+    nsum = np.zeros(N)
+    nsum[:-1] += off
+    nsum[1:] += off
+    diag = np.where(diag >= nsum, diag, nsum)
+    diag[0] = 2.0 * off[0]
+    diag[-1] = 2.0 * off[-1]
+    i = np.arange(N)
+    rows = np.concatenate([i, i[:-1], i[1:]])
+    cols = np.concatenate([i, i[1:], i[:-1]])
+    A = SparseMatrix.from_coo(N, rows, cols, np.concatenate([diag, off, off]), device=device)
+    return ProblemInstance(A=A, b=np.ones(N), x0=np.zeros(N), stopping_norm=ABSOLUTE_L2,
+                           cjm_bounds=None, label=f"tridiag:{N}:seed{seed}")
+
+
+def laplace_2d_neumann(n: int, seed: int, device=None) -> ProblemInstance:
+    """2D Laplace with homogeneous Neumann faces, A x = 0 (reference
+    problems.py:101-145): ghost nodes reflect onto the inward neighbour and
+    boundary rows are scaled by 1/2 per boundary direction (symmetric, same
+    Jacobi iteration); x0 uniform in [0, 1) from SplitMix64(seed); judged on
+    the solution-difference infinity norm."""
+    from .sparse import SparseMatrix
+    if n < 2:
+        raise ValueError("n must be at least 2")
+    dx = 1.0 / (n + 1)
+    dx2 = 1.0 / dx ** 2
+    jj, ii = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    ii, jj = ii.ravel(), jj.ravel()
+    wt = np.where((ii == 0) | (ii == n - 1), 0.5, 1.0) * np.where((jj == 0) | (jj == n - 1),
+                                                                  0.5, 1.0)
+    k = ii + n * jj
+    rows, cols, vals = [k], [k], [4.0 * wt * dx2]
+    for di, dj in ((1, 0), (-1, 0), (0, 1), (0, -1)):
+        ni, nj = ii + di, jj + dj
+        inside = (ni >= 0) & (ni < n) & (nj >= 0) & (nj < n)
+        ci = np.where(inside, ni, ii - di)   # ghost reflects to the inward neighbour
+        cj = np.where(inside, nj, jj - dj)
+        rows.append(k)
+        cols.append(ci + n * cj)
+        vals.append(-wt * dx2)
+    A = SparseMatrix.from_coo(n * n, np.concatenate(rows), np.concatenate(cols),
+                              np.concatenate(vals), device=device)
+    mu = (np.cos(np.pi * dx) + 1.0) / 2.0
+    return ProblemInstance(A=A, b=np.zeros(n * n), x0=uniforms_counter(seed, n * n),
+                           stopping_norm=SOLUTION_DIFF_INF, cjm_bounds=(-mu, mu),
+                           label=f"laplace2d:{n}:seed{seed}")
+
+
+# ---------------------------------------------------------------------------
 # Config 4: variable-coefficient diffusion -div(k grad u) = f on n x n
 # ---------------------------------------------------------------------------
 

@@ -23,7 +23,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .operators import Field, StencilOperator
+from .operators import DeviceOperator, Field, StencilOperator
 from .problems import ABSOLUTE_L2, RELATIVE_L2, SOLUTION_DIFF_INF, ProblemInstance
 from .schemes import (MAX_LEVEL, ORDER_GRID_SIZE, SrjScheme, generate_srj_scheme,
                       scheme_for_level)
@@ -190,30 +190,79 @@ class _OmegaCache:
 _OMEGAS = _OmegaCache()
 
 
-def _require_device_operator(A) -> StencilOperator:
-    if not isinstance(A, StencilOperator):
+def _require_device_operator(A) -> DeviceOperator:
+    if not isinstance(A, DeviceOperator):
         raise TypeError(
-            "the SRJ device path needs a StencilOperator (structured 1D/2D/3D stencil); "
-            f"got {type(A).__name__}")
+            "the SRJ device path needs a device operator (StencilOperator or "
+            f"sparse.SparseMatrix); got {type(A).__name__}")
     return A
 
 
 def _l2_norm_parts(norm: str) -> None:
-    if norm == SOLUTION_DIFF_INF:
-        raise NotImplementedError(
-            "solution_diff_inf stopping is not on the device path yet (SURVEY §8 f2)")
-    if norm not in (ABSOLUTE_L2, RELATIVE_L2):
+    if norm not in (ABSOLUTE_L2, RELATIVE_L2, SOLUTION_DIFF_INF):
         raise ValueError(f"unknown norm {norm!r}")
 
 
-def _device_cycle(A: StencilOperator, b: Field, x: Field, x_alt: Field, state: SolverState,
+def _diff_cycle(A, b, x, x_alt, state, scheme, stopping, record_history, x_out_kind):
+    """One cycle under the solution-difference infinity norm, step for step
+    reference solver.py:200-203,216-273 with diff_norm true; the sweep loop is
+    srj_run_cycle_diffinf (norm bit-identical: a max)."""
+    res_now = state.current_residual
+    res_before = res_now
+    history = list(state.residual_history) if record_history else state.residual_history
+    M = scheme.M
+    tol = stopping.tolerance if stopping is not None else -1.0
+    budget = (stopping.max_iterations - state.total_iterations) if stopping is not None else M
+    # the first sweep's norm becomes res_before when none is known (:242-243)
+    hist = np.empty(M, dtype=np.float64) if (record_history or res_now is None) else None
+    omegas = _OMEGAS.get(scheme, A.device)
+    out = A.run_cycle_diffinf(x, x_alt, b, omegas, M, tol, res_now, budget, hist)
+    executed = int(out.executed)
+    if out.status == _lib.CYCLE_DIVERGED:
+        raise SolveDivergedError({
+            "cycle": state.cycle_index, "sweep": executed,
+            "omega": scheme.ordered_omegas()[executed - 1], "level": scheme.level, "M": scheme.M,
+        })
+    if executed > 0:
+        res_now = float(out.res_after)
+        if res_before is None:
+            res_before = float(hist[0])
+    if record_history and executed:
+        base = state.total_iterations
+        history.extend((base + k + 1, float(hist[k])) for k in range(executed))
+    res_after = res_now if res_now is not None else float("nan")
+    if res_before is None:
+        res_before = res_after
+    converged = stopping is not None and res_now is not None and res_now <= stopping.tolerance
+    if executed > 0 and res_before > 0.0 and res_after > 0.0:
+        rate = average_convergence_rate(res_before, res_after, executed)
+        ratio = res_after / res_before
+    else:
+        rate = math.inf if executed > 0 else 0.0
+        ratio = state.prev_residual_ratio
+    result, other = (x_alt, x) if out.result_in_alt else (x, x_alt)
+    stats = CycleStats(
+        cycle=state.cycle_index, level=scheme.level if scheme.level is not None else -1,
+        M=scheme.M, executed=executed, residual_before=res_before, residual_after=res_after,
+        average_rate=rate)
+    new_state = SolverState(
+        x=x_out_kind(result), level=scheme.level if scheme.level is not None else state.level,
+        prev_residual_ratio=ratio if executed > 0 else state.prev_residual_ratio,
+        cycle_index=state.cycle_index + 1, total_iterations=state.total_iterations + executed,
+        residual_history=history, current_residual=res_now, cached_r=None, converged=converged)
+    return new_state, stats, result, other
+
+
+def _device_cycle(A: DeviceOperator, b: Field, x: Field, x_alt: Field, state: SolverState,
                   scheme: SrjScheme, stopping: StoppingRule | None, baseline: float,
-                  record_history: bool, x_out_kind):
+                  record_history: bool, x_out_kind, norm: str = ABSOLUTE_L2):
     """One cycle on (x, x_alt); returns (new_state, stats, result_field, other_field).
 
     Follows reference solver.py:187-273 step by step; the sweep loop itself
     (:216-243) is the device call.
     """
+    if norm == SOLUTION_DIFF_INF:
+        return _diff_cycle(A, b, x, x_alt, state, scheme, stopping, record_history, x_out_kind)
     if state.cached_r is not None and state.current_residual is not None:
         res_now = float(state.current_residual)
     else:
@@ -292,7 +341,7 @@ def run_cycle(A: StencilOperator, b, state: SolverState, scheme: SrjScheme,
         return f.interior.cpu().numpy() if as_numpy else f.interior
 
     new_state, stats, _, _ = _device_cycle(A, bf, x, x_alt, state, scheme, stopping,
-                                           baseline, record_history, kind)
+                                           baseline, record_history, kind, norm)
     return new_state, stats
 
 
@@ -359,7 +408,8 @@ def solve_fields(A: StencilOperator, b: Field, x: Field, x_alt: Field, controlle
     while True:
         scheme = _next_scheme(controller, state, order_grid)
         state, stats, x, x_alt = _device_cycle(A, b, x, x_alt, state, scheme, stopping,
-                                               baseline, record_history, _field_view)
+                                               baseline, record_history, _field_view,
+                                               stopping.norm)
         if cycle_hook is not None:
             cycle_hook(stats)
         if stats.executed > 0:

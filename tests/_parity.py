@@ -75,6 +75,38 @@ def case_inputs(c):
     return fam, n, b, fx, fy
 
 
+def is_csr(c) -> bool:
+    return c["family"].startswith("csr:")
+
+
+def csr_inputs(c):
+    """(scipy CSR, b, x0) of a general-CSR golden case: the product's
+    generators (equal to the reference's, tests/test_host.py) or the committed
+    FEM fixture written by make_golden.py."""
+    import sys
+    root = os.path.dirname(HERE)
+    if root not in sys.path:
+        sys.path.insert(0, root)
+    import scipy.sparse
+
+    import paper_2011_06636_b200 as srj
+    fam = c["family"]
+    if fam == "csr:laplace2d":
+        p = srj.laplace_2d_neumann(c["n"], c["seed"])
+    elif fam == "csr:tridiag":
+        p = srj.random_tridiagonal(c["n"], c["seed"])
+    elif fam == "csr:mesh":
+        z = np.load(os.path.join(GOLDEN, c["fixture"]))
+        n = len(z["b"])
+        csr = scipy.sparse.csr_matrix((z["data"], z["indices"], z["indptr"]), shape=(n, n))
+        return csr, z["b"], z["x0"]
+    elif fam == "csr:dense1":
+        return scipy.sparse.csr_matrix(np.array([[4.0]])), np.array([8.0]), np.array([0.0])
+    else:
+        raise KeyError(fam)
+    return p.A.scipy_csr(), np.asarray(p.b), np.asarray(p.x0)
+
+
 def golden_cycle_rows(c):
     """Per-cycle (cycle, level, M, executed) ints and the rows with residuals."""
     cyc = c["cycles"]

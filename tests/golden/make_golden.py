@@ -73,7 +73,33 @@ def varcoef_2d_ref(n: int, seed: int):
     return A, sha(fx), sha(fy)
 
 
+def build_csr(case):
+    """General-CSR problems (§8 f2/f3) through the reference's own generators."""
+    fam = case["family"]
+    if fam == "csr:laplace2d":
+        p = srj.laplace_2d_neumann(case["n"], case["seed"])
+        return p, {}
+    if fam == "csr:tridiag":
+        return srj.random_tridiagonal(case["n"], case["seed"]), {}
+    if fam == "csr:mesh":
+        from srj.problems import assemble_fem_poisson, read_mesh
+        p = assemble_fem_poisson(read_mesh(os.path.join("/root/reference/pkg/assets",
+                                                        case["mesh"] + ".mesh")))
+        csr = p.A.scipy_csr()
+        path = os.path.join(HERE, f"fem_{case['mesh']}.npz")
+        np.savez_compressed(path, indptr=csr.indptr, indices=csr.indices, data=csr.data,
+                            b=p.b, x0=p.x0)
+        return p, {"fixture": os.path.basename(path), "n": p.A.n}
+    if fam == "csr:dense1":
+        A = SparseMatrix.from_dense([[4.0]])
+        return ProblemInstance(A=A, b=np.array([8.0]), x0=np.array([0.0]),
+                               stopping_norm=case["norm"]), {}
+    raise ValueError(fam)
+
+
 def build(case):
+    if case["family"].startswith("csr:"):
+        return build_csr(case)
     fam, n, seed, rhs = case["family"], case["n"], case.get("seed", 0), case.get("rhs", "uniform")
     extra = {}
     if fam == "1d3":
@@ -239,6 +265,23 @@ CASES = [
      "tol": 1e-9, "controller": "fixed:2362"},
     {"name": "blowup_diverges", "family": "1d3", "n": 100, "rhs": "ones",
      "norm": "absolute_l2", "tol": 1e-7, "controller": "blowup"},
+    # general CSR operators (§8 f3) and the solution-difference norm (§8 f2)
+    {"name": "laplace2d_64_seed1", "family": "csr:laplace2d", "n": 64, "seed": 1,
+     "norm": "solution_diff_inf", "tol": 1e-10, "controller": "heuristic", "history": True},
+    {"name": "laplace2d_8_seed3", "family": "csr:laplace2d", "n": 8, "seed": 3,
+     "norm": "solution_diff_inf", "tol": 1e-8, "controller": "heuristic", "max_iterations": 50000},
+    {"name": "laplace2d_16_jacobi_budget", "family": "csr:laplace2d", "n": 16, "seed": 2,
+     "norm": "solution_diff_inf", "tol": 1e-12, "controller": "jacobi", "max_iterations": 300},
+    {"name": "tridiag_500_seed0", "family": "csr:tridiag", "n": 500, "seed": 0,
+     "norm": "absolute_l2", "tol": 1e-7, "controller": "heuristic"},
+    {"name": "tridiag_200_seed1_increasing", "family": "csr:tridiag", "n": 200, "seed": 1,
+     "norm": "absolute_l2", "tol": 1e-7, "controller": "increasing"},
+    {"name": "fem_disk", "family": "csr:mesh", "mesh": "disk", "n": 0,
+     "norm": "absolute_l2", "tol": 1e-9, "controller": "heuristic"},
+    {"name": "fem_airfoil_med", "family": "csr:mesh", "mesh": "airfoil_med", "n": 0,
+     "norm": "absolute_l2", "tol": 1e-9, "controller": "heuristic"},
+    {"name": "dense_1x1", "family": "csr:dense1", "n": 1, "norm": "absolute_l2", "tol": 1e-12,
+     "controller": "jacobi"},
 ]
 
 

@@ -22,16 +22,22 @@ def device_solve(c, record_history=True, sweeps_per_pass=None):
     import torch
 
     import paper_2011_06636_b200 as srj
-    fam, n, b, fx, fy = P.case_inputs(c)
-    dims = {"1d3": (n,), "2d5": (n, n), "2d5var": (n, n), "3d7": (n, n, n)}[fam]
     dev = torch.device("cuda", 0)
-    if fam == "2d5var":
-        A = srj.StencilOperator(fam, dims, face_x=fx, face_y=fy, device=dev)
+    if P.is_csr(c):
+        csr, b, x0 = P.csr_inputs(c)
+        A = srj.SparseMatrix(csr, device=dev)
+        n = A.n
     else:
-        A = srj.StencilOperator(fam, dims, device=dev)
+        fam, n, b, fx, fy = P.case_inputs(c)
+        dims = {"1d3": (n,), "2d5": (n, n), "2d5var": (n, n), "3d7": (n, n, n)}[fam]
+        if fam == "2d5var":
+            A = srj.StencilOperator(fam, dims, face_x=fx, face_y=fy, device=dev)
+        else:
+            A = srj.StencilOperator(fam, dims, device=dev)
+        x0 = np.zeros(A.n)
     if sweeps_per_pass:
         A.set_sweeps_per_pass(sweeps_per_pass)
-    p = srj.ProblemInstance(A=A, b=b, x0=np.zeros(A.n), stopping_norm=c["norm"])
+    p = srj.ProblemInstance(A=A, b=b, x0=x0, stopping_norm=c["norm"])
     ctrl = c["controller"]
     if ctrl == "heuristic":
         controller = srj.Heuristic()
@@ -128,3 +134,28 @@ def test_temporal_blocking_matches_reference(name, spp):
     rep = device_solve(c, record_history="history" in c, sweeps_per_pass=spp)
     P.assert_trace_matches(c, rows_of(rep), rep.total_iterations, rep.converged, x=rep.x,
                            history=rep.residual_history if "history" in c else None)
+
+
+def test_standalone_sweep_and_norm_helpers_match_oracle():
+    """a6: weighted_jacobi_sweep / matvec / residual norms / diff_inf on device."""
+    import paper_2011_06636_b200 as srj
+    from oracle import srj_oracle as O
+    c = P.case("tridiag_500_seed0")
+    csr, b, _ = P.csr_inputs(c)
+    A = srj.SparseMatrix(csr)
+    x = O.uniform_rhs(9, A.n)
+    orc = O.CsrCPU(csr)
+    r, s = orc.residual(x, b)
+    assert np.array_equal(srj.weighted_jacobi_sweep(A, x, b, 0.7), orc.update(x, r, 0.7))
+    assert np.array_equal(srj.matvec(A, x), csr.dot(x))
+    assert math.isclose(srj.residual_l2(A, x, b), math.sqrt(s), rel_tol=1e-13)
+    S = srj.StencilOperator("3d7", (9, 9, 9))
+    xs = O.uniform_rhs(3, S.n)
+    bs = O.uniform_rhs(4, S.n)
+    ref = O.stencil("3d7", 9)
+    rr, _ = ref.residual(xs, bs)
+    assert np.array_equal(srj.weighted_jacobi_sweep(S, xs, bs, 1.3), ref.update(xs, rr, 1.3))
+    assert np.array_equal(srj.matvec(S, xs), ref.matvec(xs))
+    assert srj.diff_inf(xs, bs) == float(np.max(np.abs(xs - bs)))
+    with pytest.raises(ValueError):
+        srj.matvec(S, xs[:-1])

@@ -164,5 +164,38 @@ def test_device_path_refuses_non_stencil_operators():
     csr_like = types.SimpleNamespace(A=types.SimpleNamespace(n=4), b=np.ones(4), x0=np.zeros(4))
     with pytest.raises(TypeError):
         srj.solve(csr_like, srj.Heuristic(), srj.StoppingRule("absolute_l2", 1e-6, 10))
-    with pytest.raises(NotImplementedError):
-        srj.solve(p, srj.Heuristic(), srj.StoppingRule("solution_diff_inf", 1e-6, 10))
+    with pytest.raises(ValueError):
+        srj.solve(p, srj.Heuristic(), srj.StoppingRule("max_norm", 1e-6, 10))
+
+
+def test_sparse_matrix_contract_matches_reference():
+    # constructor semantics of reference sparse.py:20-44 (no device needed)
+    A = srj.SparseMatrix.from_coo(3, [0, 0, 1, 1, 2, 2, 0], [0, 1, 0, 1, 2, 1, 0],
+                                  [1.0, -1.0, -1.0, 4.0, 2.0, 0.0, 1.0])
+    assert A.n == 3 and A.nnz == 6
+    assert list(A.row_ptr) == [0, 2, 4, 6]
+    assert np.array_equal(A.diag, [2.0, 4.0, 2.0])  # duplicate (0,0) entries summed
+    assert np.array_equal(A.inv_diag, 1.0 / np.array([2.0, 4.0, 2.0]))
+    with pytest.raises(ValueError, match="square"):
+        srj.SparseMatrix(np.ones((2, 3)))
+    with pytest.raises(ValueError, match="symmetric"):
+        srj.SparseMatrix.from_dense([[2.0, 1.0], [0.0, 2.0]])
+    with pytest.raises(ValueError, match="diagonal"):
+        srj.SparseMatrix.from_dense([[0.0, 1.0], [1.0, 2.0]])
+
+
+def test_csr_generators_match_reference():
+    import sys
+    sys.path.insert(0, "/root/reference/pkg/src")
+    try:
+        from srj.problems import laplace_2d_neumann, random_tridiagonal
+    except ImportError:
+        pytest.skip("reference not mounted")
+    for ours, ref in ((srj.random_tridiagonal(9, 42), random_tridiagonal(9, 42)),
+                      (srj.laplace_2d_neumann(6, 3), laplace_2d_neumann(6, 3))):
+        a, b = ours.A.scipy_csr(), ref.A.scipy_csr()
+        assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
+        assert np.array_equal(a.data, b.data)
+        assert np.array_equal(ours.A.inv_diag, ref.A.inv_diag)
+        assert np.array_equal(ours.b, ref.b) and np.array_equal(ours.x0, ref.x0)
+        assert ours.stopping_norm == ref.stopping_norm and ours.cjm_bounds == ref.cjm_bounds
