@@ -188,6 +188,25 @@ int srj_sweep_planes(srj_op* op, const double* x, double* x_out, const double* b
                      double omega, int64_t z_begin, int64_t z_end, double* partial_dev,
                      int32_t slot, void* stream);
 
+/* Batched small 1D Poisson cycles (data collection, datacollect.py:79-117:
+ * the candidate cycles of many independent trials in one launch).  Job j
+ * applies M sweeps (no stopping) of the n-point Dirichlet system
+ * (-1, 2, -1)*(n+1)^2 to x_pool[x_in_off .. +n) with b_pool[b_off .. +n) and
+ * omega_pool[omega_off .. +M), writes the final iterate to x_pool[x_out_off ..)
+ * and sum (b - A x)^2 of it to sumsq_dev[j].  jobs_dev is a device array;
+ * max_n bounds every job's n (<= 12288).  Asynchronous. */
+typedef struct srj_batch_job {
+    int32_t n;
+    int32_t M;
+    int64_t omega_off;
+    int64_t x_in_off;
+    int64_t x_out_off;
+    int64_t b_off;
+} srj_batch_job;
+int srj_batch_cycles_1d(const srj_batch_job* jobs_dev, int32_t njobs, int32_t max_n,
+                        const double* omega_pool, double* x_pool, const double* b_pool,
+                        double* sumsq_dev, int32_t device, void* stream);
+
 /* y = A x (y needs no ghosts). */
 int srj_matvec(srj_op* op, const double* x, double* y, void* stream);
 /* out[i] = 2 * u_{start+i} - 1, u_j the j-th uniform of SplitMix64(seed). */

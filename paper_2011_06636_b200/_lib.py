@@ -26,8 +26,13 @@ EXPORTED_SYMBOLS = (
     "srj_op_layout", "srj_op_diag", "srj_op_set_sweeps_per_pass", "srj_op_describe",
     "srj_residual_sq",
     "srj_run_cycle", "srj_sweep", "srj_matvec", "srj_fill_uniform_rhs",
-    "srj_op_planes", "srj_sweep_planes", "srj_run_cycle_diffinf",
+    "srj_op_planes", "srj_sweep_planes", "srj_run_cycle_diffinf", "srj_batch_cycles_1d",
 )
+
+
+class BatchJob(ctypes.Structure):
+    _fields_ = [("n", c_int32), ("M", c_int32), ("omega_off", c_int64),
+                ("x_in_off", c_int64), ("x_out_off", c_int64), ("b_off", c_int64)]
 
 
 class OpDesc(ctypes.Structure):
@@ -86,6 +91,8 @@ def _declare(L):
     L.srj_matvec.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p]
     L.srj_fill_uniform_rhs.argtypes = [c_void_p, c_int64, c_uint64, c_int64, c_int32, c_void_p]
     L.srj_op_planes.argtypes = [c_void_p]
+    L.srj_batch_cycles_1d.argtypes = [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
+                                      c_void_p, c_int32, c_void_p]
     L.srj_run_cycle_diffinf.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                         c_int32, c_double, c_double, c_int64, c_void_p,
                                         POINTER(CycleOut), c_void_p]

@@ -285,9 +285,31 @@ CASES = [
 ]
 
 
+def datacollect_cases():
+    """Reference data collection (datacollect.py:79-147) and the threshold fit."""
+    from srj import datacollect as dc
+
+    def pack(points):
+        return {"ints": [[p.trial, p.step, dc.ACTIONS.index(p.action), p.level] for p in points],
+                "reals": [[p.avg_rate, p.prev_ratio, p.res_before, p.res_after] for p in points]}
+
+    out = {
+        "collect_10_t2_s5": pack(dc.collect([10], 2, target_tol=1e-8, seed=5)),
+        "collect_5_30_t2_s7": pack(dc.collect([5, 30], 2, target_tol=1e-8, seed=7)),
+        "until_5_10_200_s2": pack(dc.collect_until([5, 10], 200, target_tol=1e-6, seed=2)),
+    }
+    pts = dc.collect_until([10, 50], 40000, seed=3)
+    clusters = dc.aggregate(pts, n_set=1000)
+    t_hi, t_lo = dc.fit_thresholds(clusters)
+    out["fit_10_50_40000_s3"] = {
+        "count": len(pts), "t_hi": t_hi, "t_lo": t_lo,
+        "clusters": [[c.level_bucket, c.mean_ratio, c.best_action] for c in clusters]}
+    return out
+
+
 def main():
     traces = {"reference": "/root/reference (srj 0.1.0)", "numpy": np.__version__,
-              "cases": [], "run_cycle": run_cycle_cases()}
+              "cases": [], "run_cycle": run_cycle_cases(), "datacollect": datacollect_cases()}
     for case in CASES:
         print("running", case["name"], flush=True)
         traces["cases"].append(run_case(case))
