@@ -139,8 +139,17 @@ enum srj_cycle_kernel {
     SRJ_KERNEL_GENERIC = 0,    /* persistent row walker (any family)            */
     SRJ_KERNEL_TB2D = 1,       /* temporally blocked 2D (sweeps_per_pass > 1)   */
     SRJ_KERNEL_TILE2D = 2,     /* TMA tile streaming 2D (constant / variable)   */
-    SRJ_KERNEL_PLANE3D = 3     /* TMA plane streaming 3D                        */
+    SRJ_KERNEL_PLANE3D = 3,    /* TMA plane streaming 3D                        */
+    SRJ_KERNEL_WS2D = 4        /* warp-streaming temporal blocking 2D           */
 };
+
+/* Temporally blocked 2D kernel used when sweeps_per_pass > 1. */
+enum srj_tb_kind {
+    SRJ_TB_TILE = 0,           /* TMA-staged overlapped tiles (srj_tb.cu), default */
+    SRJ_TB_WARP_STREAM = 1     /* barrier-free warp streaming (srj_ws2d.cu),
+                                  experimental, <= 4 sweeps per pass              */
+};
+int srj_op_set_temporal_kernel(srj_op* op, int32_t kind);
 int srj_op_describe(const srj_op* op, srj_op_info* info);
 
 /* sum_i (b - A x)_i^2 -> *sumsq_host.  Synchronises `stream`. */

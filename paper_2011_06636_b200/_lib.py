@@ -27,7 +27,9 @@ EXPORTED_SYMBOLS = (
     "srj_residual_sq",
     "srj_run_cycle", "srj_sweep", "srj_matvec", "srj_fill_uniform_rhs",
     "srj_op_planes", "srj_sweep_planes", "srj_run_cycle_diffinf", "srj_batch_cycles_1d",
+    "srj_op_set_temporal_kernel",
 )
+TB_TILE, TB_WARP_STREAM = 0, 1
 
 
 class BatchJob(ctypes.Structure):
@@ -61,7 +63,8 @@ class OpInfo(ctypes.Structure):
     KERNELS = {0: "srj::k_cycle (generic row walker)",
                1: "srj::k_tb2d_cycle (TMA temporal blocking)",
                2: "srj::k_cycle2d (TMA tile streaming)",
-               3: "srj::k_cycle3d (TMA plane ring)"}
+               3: "srj::k_cycle3d (TMA plane ring)",
+               4: "srj::k_ws2d_cycle (warp-streaming temporal blocking)"}
 
     def as_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
@@ -91,6 +94,7 @@ def _declare(L):
     L.srj_matvec.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p]
     L.srj_fill_uniform_rhs.argtypes = [c_void_p, c_int64, c_uint64, c_int64, c_int32, c_void_p]
     L.srj_op_planes.argtypes = [c_void_p]
+    L.srj_op_set_temporal_kernel.argtypes = [c_void_p, c_int32]
     L.srj_batch_cycles_1d.argtypes = [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
                                       c_void_p, c_int32, c_void_p]
     L.srj_run_cycle_diffinf.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

@@ -26,6 +26,7 @@
 #include "srj_stencil.cuh"
 #include "srj_2d.cuh"
 #include "srj_3d.cuh"
+#include "srj_ws2d.cuh"
 #include "srj_tb.cuh"
 #include "srj_walk.cuh"
 
@@ -221,6 +222,8 @@ struct srj_op {
     TbPlan tb;                   // temporal-blocking plan (srj_tb.cuh)
     Plan3D p3;                   // plane-streaming 3D plan (srj_3d.cuh)
     Plan2D p2;                   // tile-streaming 2D plan (srj_2d.cuh)
+    WsPlan ws;                   // warp-streaming temporal blocking (srj_ws2d.cuh)
+    int tb_kind = SRJ_TB_TILE;   // measured faster on B200
     // srj_sweep_planes scratch, one set per slot (concurrent launches)
     double* slot_part[kSlots] = {nullptr, nullptr};
     unsigned* slot_counter = nullptr;  // device [kSlots], zero between launches
@@ -346,6 +349,11 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("allocation failed: ") + cudaGetErrorString(e));
     }
+    if ((e = ws_plan_init(op->ws, g, op->num_sms)) != cudaSuccess) {
+        srj_op_destroy(op);
+        return fail(SRJ_CUDA_ERROR, std::string("warp-stream plan setup failed: ") + cudaGetErrorString(e));
+    }
+    if (const char* kind = getenv("SRJ_TB_KIND")) op->tb_kind = atoi(kind);
     if ((e = plan2d_init(op->p2, g, op->num_sms)) != cudaSuccess) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("2D plan setup failed: ") + cudaGetErrorString(e));
@@ -360,7 +368,7 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
     }
     // Default: 4 sweeps per pass where a temporally blocked kernel exists
     // (measured best on B200 for 2D), else one per pass.
-    op->sweeps_per_pass = op->tb.supported ? 4 : 1;
+    op->sweeps_per_pass = (op->tb.supported || op->ws.supported) ? 4 : 1;
     op->slot_capacity = std::max(op->p3.slots, kApplyBlocksPerSm * op->num_sms);
     for (int s = 0; s < kSlots; ++s) {
         if ((e = cudaMalloc(&op->slot_part[s], op->slot_capacity * sizeof(double))) != cudaSuccess) {
@@ -410,6 +418,14 @@ int srj_op_diag(const srj_op* op, double* diag, double* inv_diag) {
     return SRJ_OK;
 }
 
+int srj_op_set_temporal_kernel(srj_op* op, int32_t kind) {
+    if (!op) return fail(SRJ_BAD_ARGUMENT, "null operator");
+    if (kind != SRJ_TB_TILE && kind != SRJ_TB_WARP_STREAM)
+        return fail(SRJ_BAD_ARGUMENT, "unknown temporal-blocking kernel");
+    op->tb_kind = kind;
+    return SRJ_OK;
+}
+
 int srj_op_describe(const srj_op* op, srj_op_info* info) {
     if (!op || !info) return fail(SRJ_BAD_ARGUMENT, "null argument");
     info->num_sms = op->num_sms;
@@ -421,6 +437,8 @@ int srj_op_describe(const srj_op* op, srj_op_info* info) {
     info->tb_occupancy = op->tb.occupancy;
     info->tb_tiles = op->tb.ntiles[op->tb.small_variant];
     info->cycle_kernel = op->p3.supported                                 ? SRJ_KERNEL_PLANE3D
+                         : (op->sweeps_per_pass > 1 && op->ws.supported &&
+                            op->tb_kind == SRJ_TB_WARP_STREAM) ? SRJ_KERNEL_WS2D
                          : (op->sweeps_per_pass > 1 && op->tb.supported) ? SRJ_KERNEL_TB2D
                          : op->p2.supported                               ? SRJ_KERNEL_TILE2D
                                                                           : SRJ_KERNEL_GENERIC;
@@ -502,6 +520,11 @@ int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
     if (op->p3.supported) {
         CUDA_TRY(launch3d_cycle(op->p3, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,
                                 op->partials, op->hist, op->out_i, op->out_d, st));
+        out->launches = 1;
+    } else if (op->sweeps_per_pass > 1 && op->ws.supported && op->tb_kind == SRJ_TB_WARP_STREAM) {
+        CUDA_TRY(ws_launch_cycle(op->ws, op->g, x, x_alt, b, omegas_dev, Meff,
+                                 op->sweeps_per_pass, tol, baseline, op->partials, op->hist,
+                                 op->out_i, op->out_d, st));
         out->launches = 1;
     } else if (op->sweeps_per_pass > 1 && op->tb.supported) {
         CUDA_TRY(tb_launch_cycle(op->tb, op->g, x, x_alt, b, omegas_dev, Meff,

@@ -124,6 +124,14 @@ class DeviceOperator:
         _lib.check(_lib.lib().srj_op_set_sweeps_per_pass(self.handle, int(s)),
                    "srj_op_set_sweeps_per_pass")
 
+    def set_temporal_kernel(self, kind: str) -> None:
+        """'tile' (default, TMA overlapped tiles) or 'warp_stream' (barrier-free,
+        experimental, at most 4 sweeps per pass): which temporally blocked 2D
+        kernel serves sweeps_per_pass > 1."""
+        code = {"tile": _lib.TB_TILE, "warp_stream": _lib.TB_WARP_STREAM}[kind]
+        _lib.check(_lib.lib().srj_op_set_temporal_kernel(self.handle, code),
+                   "srj_op_set_temporal_kernel")
+
     def describe(self) -> dict:
         """Launch configuration libsrj chose for this operator."""
         info = _lib.OpInfo()

@@ -18,7 +18,7 @@ import _parity as P
 pytestmark = pytest.mark.gpu
 
 
-def device_solve(c, record_history=True, sweeps_per_pass=None):
+def device_solve(c, record_history=True, sweeps_per_pass=None, tb_kind=None):
     import torch
 
     import paper_2011_06636_b200 as srj
@@ -37,6 +37,8 @@ def device_solve(c, record_history=True, sweeps_per_pass=None):
         x0 = np.zeros(A.n)
     if sweeps_per_pass:
         A.set_sweeps_per_pass(sweeps_per_pass)
+    if tb_kind:
+        A.set_temporal_kernel(tb_kind)
     p = srj.ProblemInstance(A=A, b=b, x0=x0, stopping_norm=c["norm"])
     ctrl = c["controller"]
     if ctrl == "heuristic":
@@ -127,11 +129,12 @@ def test_solve_is_deterministic_on_device():
 TB_NAMES = [c["name"] for c in P.cases(lambda c: c["family"] == "2d5" and "diverged" not in c)]
 
 
-@pytest.mark.parametrize("spp", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("kind", ["tile", "warp_stream"])
+@pytest.mark.parametrize("spp", [1, 2, 3, 5, 6, 8])
 @pytest.mark.parametrize("name", TB_NAMES)
-def test_temporal_blocking_matches_reference(name, spp):
+def test_temporal_blocking_matches_reference(name, spp, kind):
     c = P.case(name)
-    rep = device_solve(c, record_history="history" in c, sweeps_per_pass=spp)
+    rep = device_solve(c, record_history="history" in c, sweeps_per_pass=spp, tb_kind=kind)
     P.assert_trace_matches(c, rows_of(rep), rep.total_iterations, rep.converged, x=rep.x,
                            history=rep.residual_history if "history" in c else None)
 
