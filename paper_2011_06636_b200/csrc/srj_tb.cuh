@@ -16,14 +16,15 @@ struct TbPlan {
     int blocks[4] = {0, 0, 0, 0};   // cooperative grid (one CTA per SM)
     int tiles_x[4] = {0, 0, 0, 0};
     int ntiles[4] = {0, 0, 0, 0};
-    int small_variant = 2;          // variant used for s <= 4
+    int small_variant = 1;          // variant launched (tb2d::Cfg<K>)
     int occupancy = 0;              // min resident CTAs per SM over the variants
 };
 
 // Decide whether the operator has a temporal-blocking kernel and size its grid.
 cudaError_t tb_plan_init(TbPlan& plan, const Geom& g, int num_sms);
 
-// Launch one cycle of M sweeps, s per pass (1 <= s <= kTbMaxSub).  Same
+// Launch one cycle of M sweeps, s per pass (1 <= s <= kTbMaxSub; the 2D
+// kernel fuses at most 4 and clamps larger requests).  Same
 // outputs as the one-sweep cycle kernel: out_i = {executed, status, result
 // buffer (0: x, 1: x_alt)}, out_d = {final sum of squares, res_after};
 // hist[k] = relative residual of x_k for k = 1..executed.
