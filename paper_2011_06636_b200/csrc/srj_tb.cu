@@ -1,28 +1,34 @@
 // Temporally blocked SRJ cycle for the 2D 5-point constant-coefficient
-// stencil (BASELINE config 2): up to S = 4 consecutive sweeps, each with its
-// own omega, per HBM/L2 round trip of x and b.
+// stencil (BASELINE config 2): S = 4 consecutive sweeps, each with its own
+// omega, per HBM/L2 round trip of x and b.
 //
-// Tiling.  A CTA (one per SM, persistent, cooperative launch) owns TX x 64
-// output tiles.  For each tile the copy engine (TMA) brings the
-// (TX+2S) x (64+2S) region of x_{k0} and b into shared memory; boxes that stick
-// out of the grid are zero-filled, which is the Dirichlet ghost.  The next
-// tile's boxes are prefetched (b double-buffered) while the current one
-// computes.
+// Tiling.  A CTA (one per SM, persistent, cooperative launch) owns TX x TY
+// output tiles.  For each tile the copy engine (TMA) brings the RX x RY region
+// (the tile plus an S-wide ring) of x_{k0} and b into shared memory; boxes that
+// stick out of the grid are zero-filled, which is the Dirichlet ghost.  Both
+// are moved into registers at once, and the next tile's boxes are loaded
+// into the same stage while the current tile computes.
+//
+// Register tiling.  Warp w owns rows [w*V, w*V+V) of the region; lane l owns
+// columns [l*CW, l*CW+CW) of them.  x, b and p = c_off*x of those CW*V points
+// live in registers for all S sub-sweeps.  Neighbours:
+//   west/east  -- registers, or a warp shuffle across the lane boundary;
+//   north/south -- registers, or the halo rows the warps above/below publish
+//                  in shared memory (double-buffered by sub-sweep parity,
+//                  one __syncthreads per sub-sweep).
+// Measured on B200 (tools/probe/rates_probe.cu): a 64-bit warp shuffle costs
+// ~1/3 of the shared-memory bandwidth an LDS.64 exchange needs, so the only
+// shared traffic left is the staging load and the halo rows.
 //
 // Shared products.  With constant coefficients the rounded product
-// p_j = c_off * x_j is the same value for all four points that have x_j as a
-// neighbour, so each point computes p once when its value is produced and
-// publishes p (not x) to the exchange buffer:
+// p_j = c_off*x_j is the same value for all four points that have x_j as a
+// neighbour, so it is computed once per point and sub-sweep:
 //     y = ((((0 + p_s) + p_w) + c_diag*x) + p_e) + p_n
-// is bit-identical to summing freshly rounded products (reference csr_matvec
-// order), and costs 11 fp64 instructions per point-sweep instead of 15.
+// is bit-identical to the reference csr_matvec order with freshly rounded
+// products; 11 fp64 instructions per point-sweep.
 //
-// Register tiling.  Thread (c, seg) keeps x and p of rows [seg*V, seg*V+V) of
-// region column c in registers; per sub-sweep it reads its west/east
-// neighbours' p and the p of one row above and below its segment from the
-// exchange buffer, b from the staged tile, and publishes its new p.  Every
-// region point is updated every sub-sweep; values within t+1 rings of the
-// region edge are garbage after sub-sweep t but never reach the owned tile,
+// Every region point is updated every sub-sweep; values within t+1 rings of
+// the region edge are garbage after sub-sweep t but never reach the owned tile,
 // which after h <= S sub-sweeps holds x_{k0+h} exactly (bit-identical
 // iterates).  Grid-exterior points are held at 0.
 //
@@ -45,35 +51,37 @@
 namespace srj {
 namespace tb2d {
 
-template <int S_, int TX_, int TY_, int NSEG_>
+template <int S_, int CW_, int V_, int NSEG_>
 struct CfgBase {
-    static constexpr int S = S_, TX = TX_, TY = TY_;
-    static constexpr int RX = TX + 2 * S, RY = TY + 2 * S;
-    static constexpr int NSEG = NSEG_;
-    static constexpr int V = RY / NSEG;
-    static_assert(RY % NSEG == 0, "segments must tile the region height");
-    static constexpr int THREADS = RX * NSEG;
+    static constexpr int S = S_;        // sweeps fused per pass (= ring width)
+    static constexpr int CW = CW_;      // columns per lane
+    static constexpr int V = V_;        // rows per warp
+    static constexpr int NSEG = NSEG_;  // warps
+    static constexpr int RX = 32 * CW, RY = NSEG * V;
+    static constexpr int TX = RX - 2 * S, TY = RY - 2 * S;
+    static_assert(CW * V <= 32, "point masks are 32-bit");
+    static_assert(TX % 2 == 0, "tile origins must stay 16-byte aligned for TMA");
+    static constexpr int THREADS = 32 * NSEG;
     // Registers are allocated per SM sub-partition (16K each, 4 per SM): with
     // W warps, ceil(W/4) warps share one.
-    static constexpr int WARPS_PER_SMSP = ((THREADS + 31) / 32 + 3) / 4;
+    static constexpr int WARPS_PER_SMSP = (NSEG + 3) / 4;
     static constexpr int MAXREG_RAW = (16384 / (WARPS_PER_SMSP * 32)) / 8 * 8;
     static constexpr int MAXREG = MAXREG_RAW > 255 ? 255 : MAXREG_RAW;
-    static constexpr int EP = RX + 2;        // exchange buffer pitch (border columns)
-    static constexpr int EROWS = RY + 2;
-    static constexpr int STAGE = RX * RY;    // doubles per staged box
-    static constexpr int EX = EP * EROWS;    // doubles per exchange buffer
-    // x stage, two b stages, two exchange buffers, one mbarrier per b stage
-    static constexpr size_t SMEM = (size_t)(3 * STAGE + 2 * EX) * sizeof(double) + 32;
+    static constexpr int STAGE = RX * RY;          // doubles per staged box
+    static constexpr int HROWS = NSEG + 2;         // halo rows incl. a zero row each side
+    static constexpr int HBUF = 2 * HROWS * RX;    // top + bottom rows, one parity
+    // x stage, b stage, halo rows [2 parities], one mbarrier
+    static constexpr size_t SMEM = (size_t)(2 * STAGE + 2 * HBUF) * sizeof(double) + 16;
     static constexpr uint32_t TX_BYTES = 2u * STAGE * sizeof(double);
 };
 
-// Kernel variants: K -> (sweeps per pass S, owned tile TX x TY, segments).
+// Kernel variants: K -> (S, columns per lane, rows per warp, warps).
 template <int K>
 struct Cfg;
 template <>
-struct Cfg<0> : CfgBase<4, 64, 64, 8> {};  // 72x72 region, 576 threads
+struct Cfg<0> : CfgBase<4, 2, 6, 12> {};  // 64x72 region, 56x64 tile, 384 threads
 template <>
-struct Cfg<1> : CfgBase<4, 56, 64, 8> {};  // 64x72 region, 512 threads
+struct Cfg<1> : CfgBase<4, 4, 6, 12> {};  // 128x72 region, 120x64 tile, 384 threads
 constexpr int kVariants = 2;
 
 }  // namespace tb2d
@@ -101,87 +109,119 @@ extern __shared__ __align__(128) double tb_smem[];
 template <int K>
 struct TbLayout {
     using C = tb2d::Cfg<K>;
-    static constexpr int STX = 0;                  // x stage
-    static constexpr int STB = C::STAGE;           // b stages [2]
-    static constexpr int E0 = 3 * C::STAGE;        // exchange buffers
-    static constexpr int E1 = E0 + C::EX;
-    static constexpr int BAR = E1 + C::EX;         // mbarriers [2] (one per b stage)
+    static constexpr int STX = 0, STB = C::STAGE, H = 2 * C::STAGE, BAR = H + 2 * C::HBUF;
     __device__ static __forceinline__ double* stx() { return tb_smem + STX; }
-    __device__ static __forceinline__ double* stb(int slot) { return tb_smem + STB + slot * C::STAGE; }
-    __device__ static __forceinline__ double* e(int t) { return tb_smem + ((t & 1) ? E1 : E0); }
-    __device__ static __forceinline__ uint64_t* bar(int slot) {
-        return reinterpret_cast<uint64_t*>(tb_smem + BAR) + slot;
+    __device__ static __forceinline__ double* stb() { return tb_smem + STB; }
+    // halo rows of parity t: top rows then bottom rows, row index = warp + 1
+    __device__ static __forceinline__ double* top(int t) { return tb_smem + H + (t & 1) * C::HBUF; }
+    __device__ static __forceinline__ double* bot(int t) {
+        return tb_smem + H + (t & 1) * C::HBUF + C::HROWS * C::RX;
+    }
+    __device__ static __forceinline__ uint64_t* bar() {
+        return reinterpret_cast<uint64_t*>(tb_smem + BAR);
     }
 };
 
+// CW contiguous doubles at a 16-byte aligned shared address.
+template <int CW>
+__device__ __forceinline__ void lds_cols(double (&d)[CW], const double* p) {
+#pragma unroll
+    for (int j = 0; j < CW; j += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(p + j);
+        d[j] = v.x;
+        d[j + 1] = v.y;
+    }
+}
+template <int CW>
+__device__ __forceinline__ void sts_cols(double* p, const double (&d)[CW]) {
+#pragma unroll
+    for (int j = 0; j < CW; j += 2) *reinterpret_cast<double2*>(p + j) = make_double2(d[j], d[j + 1]);
+}
+
 template <int K>
 __device__ __forceinline__ void tb2d_issue(const TbArgs& a, const CUtensorMap* tm_in,
-                                           const CUtensorMap* tm_b, int q, int slot) {
+                                           const CUtensorMap* tm_b, int q) {
     using C = tb2d::Cfg<K>;
     using L = TbLayout<K>;
     constexpr int S = C::S;
     const int ox = (q % a.tiles_x) * C::TX, oy = (q / a.tiles_x) * C::TY;
     fence_proxy_async();
-    mbar_expect_tx(L::bar(slot), C::TX_BYTES);
-    tma_load_2d(L::stx(), tm_in, ox - S, oy - S, L::bar(slot));
-    tma_load_2d(L::stb(slot), tm_b, ox - S, oy - S, L::bar(slot));
+    mbar_expect_tx(L::bar(), C::TX_BYTES);
+    tma_load_2d(L::stx(), tm_in, ox - S, oy - S, L::bar());
+    tma_load_2d(L::stb(), tm_b, ox - S, oy - S, L::bar());
 }
 
-// H sub-sweeps (compile-time, H <= S) of the staged tile: xr/pr hold this
-// thread's x and p = c_off*x, the exchange buffer E0 holds everyone's p.
-// MASKED tiles reach outside the grid: points there (bit clear in `inmask`)
-// are held at 0.  Points with a bit set in `accmask` add r^2 to acc[t].
-template <int K, int H, bool MASKED>
-__device__ __forceinline__ void tile_sweeps(double (&xr)[tb2d::Cfg<K>::V],
-                                            double (&pr)[tb2d::Cfg<K>::V], int slot,
-                                            const double* omegas,
-                                            const Geom& g, int r0, int c, unsigned inmask,
-                                            unsigned accmask, double (&acc)[tb2d::Cfg<K>::S]) {
+template <int K>
+struct TileRegs {
     using C = tb2d::Cfg<K>;
-    constexpr int V = C::V, EP = C::EP, RX = C::RX;
-    const double coff = g.c_off, cdiag = g.c_diag, inv = g.inv_diag;
+    double x[C::V][C::CW], p[C::V][C::CW], b[C::V][C::CW];
+};
+
+// H sub-sweeps (compile-time, H <= S) of the tile held in registers.  MASKED
+// tiles reach outside the grid: points there (bit clear in `inmask`, bit
+// v*CW+j) are held at 0.  Points with a bit set in `accmask` add r^2 to acc[t].
+template <int K, int H, bool MASKED>
+__device__ __forceinline__ void tile_sweeps(TileRegs<K>& R, const double* omegas, const Geom& g,
+                                            int warp, int lane, unsigned inmask, unsigned accmask,
+                                            double (&acc)[tb2d::Cfg<K>::S]) {
+    using C = tb2d::Cfg<K>;
     using L = TbLayout<K>;
-    const double* bcol = L::stb(slot) + r0 * RX + c;
+    constexpr int V = C::V, CW = C::CW, RX = C::RX;
+    const double coff = g.c_off, cdiag = g.c_diag, inv = g.inv_diag;
+    const int col = lane * CW;
 #pragma unroll
     for (int t = 0; t < H; ++t) {
         const double w = __ldg(omegas + t);
-        const double* Ein = L::e(t);
-        double* Eout = L::e(t + 1);
-        const double* base = Ein + (r0 + 1) * EP + c;
-        double south = base[1 - EP];            // p of the row above the segment
-        const double north_end = base[V * EP + 1];  // p of the row below it
-        double* obase = Eout + (r0 + 1) * EP + c + 1;
+        double hs[CW], hn[CW];  // p of the rows above / below this warp's rows
+        lds_cols<CW>(hs, L::bot(t) + warp * RX + col);        // bottom row of warp-1
+        lds_cols<CW>(hn, L::top(t) + (warp + 2) * RX + col);  // top row of warp+1
+        double pw[V], pe[V];  // p across the lane boundary
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            const double pn = v == V - 1 ? north_end : pr[v + 1];
-            double y = DADD(0.0, south);
-            y = DADD(y, base[v * EP]);
-            y = DADD(y, DMUL(cdiag, xr[v]));
-            y = DADD(y, base[v * EP + 2]);
-            y = DADD(y, pn);
-            const double rr = DSUB(bcol[v * RX], y);
-            const double xn = relax(xr[v], inv, rr, w);
-            if ((accmask >> v) & 1u) acc[t] = fma(rr, rr, acc[t]);
-            south = pr[v];  // old p of row v: the south neighbour of row v+1
-            xr[v] = (!MASKED || ((inmask >> v) & 1u)) ? xn : 0.0;
-            pr[v] = DMUL(coff, xr[v]);
-            obase[v * EP] = pr[v];
+            pw[v] = __shfl_up_sync(0xffffffffu, R.p[v][CW - 1], 1);
+            pe[v] = __shfl_down_sync(0xffffffffu, R.p[v][0], 1);
         }
-        __syncthreads();
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+#pragma unroll
+            for (int j = 0; j < CW; ++j) {
+                const double ps = v == 0 ? hs[j] : R.p[v - 1][j];
+                const double pwv = j == 0 ? pw[v] : R.p[v][j - 1];
+                const double pev = j == CW - 1 ? pe[v] : R.p[v][j + 1];
+                const double pn = v == V - 1 ? hn[j] : R.p[v + 1][j];
+                double y = DADD(0.0, ps);
+                y = DADD(y, pwv);
+                y = DADD(y, DMUL(cdiag, R.x[v][j]));
+                y = DADD(y, pev);
+                y = DADD(y, pn);
+                const double rr = DSUB(R.b[v][j], y);
+                const double xn = relax(R.x[v][j], inv, rr, w);
+                const int bit = v * CW + j;
+                if ((accmask >> bit) & 1u) acc[t] = fma(rr, rr, acc[t]);
+                R.x[v][j] = (!MASKED || ((inmask >> bit) & 1u)) ? xn : 0.0;
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+#pragma unroll
+            for (int j = 0; j < CW; ++j) R.p[v][j] = DMUL(coff, R.x[v][j]);
+        if (t + 1 < H) {
+            sts_cols<CW>(L::top(t + 1) + (warp + 1) * RX + col, R.p[0]);
+            sts_cols<CW>(L::bot(t + 1) + (warp + 1) * RX + col, R.p[V - 1]);
+            __syncthreads();
+        }
     }
 }
 
 template <int K, bool MASKED>
-__device__ __forceinline__ void tile_dispatch(int h, double (&xr)[tb2d::Cfg<K>::V],
-                                              double (&pr)[tb2d::Cfg<K>::V], int slot,
-                                              const double* omegas,
-                                              const Geom& g, int r0, int c, unsigned inmask,
+__device__ __forceinline__ void tile_dispatch(int h, TileRegs<K>& R, const double* omegas,
+                                              const Geom& g, int warp, int lane, unsigned inmask,
                                               unsigned accmask, double (&acc)[tb2d::Cfg<K>::S]) {
     constexpr int S = tb2d::Cfg<K>::S;
 #define SRJ_TB_CASE(H)                                                                      \
     case H:                                                                                 \
         if constexpr (H <= S)                                                               \
-            tile_sweeps<K, H, MASKED>(xr, pr, slot, omegas, g, r0, c, inmask, accmask, acc); \
+            tile_sweeps<K, H, MASKED>(R, omegas, g, warp, lane, inmask, accmask, acc);      \
         break;
     switch (h) {
         SRJ_TB_CASE(1)
@@ -194,98 +234,112 @@ __device__ __forceinline__ void tile_dispatch(int h, double (&xr)[tb2d::Cfg<K>::
 }
 
 // One pass (h sub-sweeps, h <= S) over every tile this CTA owns.  If
-// `first_issued`, the TMA for this CTA's first tile is already in flight in
-// b slot `slot`.
+// `first_issued`, the TMA for this CTA's first tile is already in flight.
 template <int K>
 __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm_in,
                                           const CUtensorMap* tm_b, double* __restrict__ xout,
                                           int k0, int h, double (&acc)[tb2d::Cfg<K>::S],
-                                          bool accumulate, unsigned ownmask, uint32_t& phase, int& slot, bool first_issued) {
+                                          bool accumulate, unsigned ownmask, uint32_t& phase,
+                                          bool first_issued) {
     using C = tb2d::Cfg<K>;
     using L = TbLayout<K>;
-    constexpr int S = C::S;
-    constexpr int V = C::V, RX = C::RX, EP = C::EP;
-    const int tid = threadIdx.x;
-    const int c = tid % RX, seg = tid / RX, r0 = seg * V;
+    constexpr int S = C::S, V = C::V, CW = C::CW, RX = C::RX;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c0 = lane * CW, r0 = warp * V;
     const int nx = a.g.nx, ny = a.g.ny;
     const double coff = a.g.c_off;
     if ((int)blockIdx.x >= a.ntiles) return;
-    if (tid == 0 && !first_issued) tb2d_issue<K>(a, tm_in, tm_b, blockIdx.x, slot);
+    if (threadIdx.x == 0 && !first_issued) tb2d_issue<K>(a, tm_in, tm_b, blockIdx.x);
     for (int q = blockIdx.x; q < a.ntiles; q += gridDim.x) {
         const int ox = (q % a.tiles_x) * C::TX, oy = (q / a.tiles_x) * C::TY;
-        const int gx = ox - S + c;
+        const int gx0 = ox - S + c0;
         const int gy0 = oy - S + r0;
         const bool masked = ox < S || oy < S || ox + C::TX + S > nx || oy + C::TY + S > ny;
-        unsigned inmask = (1u << V) - 1u;
+        unsigned inmask = 0xffffffffu;
         if (masked) {
             inmask = 0u;
-            if (gx >= 0 && gx < nx) {
 #pragma unroll
-                for (int v = 0; v < V; ++v)
-                    if (gy0 + v >= 0 && gy0 + v < ny) inmask |= 1u << v;
-            }
+            for (int v = 0; v < V; ++v)
+#pragma unroll
+                for (int j = 0; j < CW; ++j)
+                    if (gy0 + v >= 0 && gy0 + v < ny && gx0 + j >= 0 && gx0 + j < nx)
+                        inmask |= 1u << (v * CW + j);
         }
         const unsigned storemask = ownmask & inmask;
         const unsigned accmask = accumulate ? storemask : 0u;
-        mbar_wait(L::bar(slot), (phase >> slot) & 1u);
-        phase ^= 1u << slot;
-        double xr[V], pr[V];
+        mbar_wait(L::bar(), phase);
+        phase ^= 1u;
+        TileRegs<K> R;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            xr[v] = L::stx()[(r0 + v) * RX + c];
-            pr[v] = DMUL(coff, xr[v]);
-            L::e(0)[(r0 + v + 1) * EP + c + 1] = pr[v];
+            lds_cols<CW>(R.x[v], L::stx() + (r0 + v) * RX + c0);
+            lds_cols<CW>(R.b[v], L::stb() + (r0 + v) * RX + c0);
+#pragma unroll
+            for (int j = 0; j < CW; ++j) R.p[v][j] = DMUL(coff, R.x[v][j]);
         }
-        __syncthreads();  // x staging consumed, E0 published
-        if (tid == 0 && q + (int)gridDim.x < a.ntiles)
-            tb2d_issue<K>(a, tm_in, tm_b, q + gridDim.x, slot ^ 1);
+        sts_cols<CW>(L::top(0) + (warp + 1) * RX + c0, R.p[0]);
+        sts_cols<CW>(L::bot(0) + (warp + 1) * RX + c0, R.p[V - 1]);
+        __syncthreads();  // stage consumed, halo rows published
+        if (threadIdx.x == 0 && q + (int)gridDim.x < a.ntiles)
+            tb2d_issue<K>(a, tm_in, tm_b, q + gridDim.x);
         if (masked)
-            tile_dispatch<K, true>(h, xr, pr, slot, a.omegas + k0, a.g, r0, c, inmask, accmask,
-                                   acc);
+            tile_dispatch<K, true>(h, R, a.omegas + k0, a.g, warp, lane, inmask, accmask, acc);
         else
-            tile_dispatch<K, false>(h, xr, pr, slot, a.omegas + k0, a.g, r0, c, inmask, accmask,
-                                    acc);
+            tile_dispatch<K, false>(h, R, a.omegas + k0, a.g, warp, lane, inmask, accmask, acc);
         if (storemask) {
 #pragma unroll
-            for (int v = 0; v < V; ++v)
-                if ((storemask >> v) & 1u) xout[(long long)(gy0 + v) * nx + gx] = xr[v];
+            for (int v = 0; v < V; ++v) {
+                double* row = xout + (long long)(gy0 + v) * nx + gx0;
+#pragma unroll
+                for (int j = 0; j < CW; j += 2) {
+                    const unsigned m2 = (storemask >> (v * CW + j)) & 3u;
+                    if (m2 == 3u)
+                        *reinterpret_cast<double2*>(row + j) = make_double2(R.x[v][j], R.x[v][j + 1]);
+                    else if (m2 == 1u)
+                        row[j] = R.x[v][j];
+                    else if (m2 == 2u)
+                        row[j + 1] = R.x[v][j + 1];
+                }
+            }
         }
-        slot ^= 1;
+        // The halo rows of parity 0 are rewritten by the next tile: make sure
+        // every warp has finished reading this tile's last halos.
+        __syncthreads();
     }
 }
 
 template <int K>
-__global__ void __maxnreg__(tb2d::Cfg<K>::MAXREG)
+__global__ void __launch_bounds__(tb2d::Cfg<K>::THREADS, 1) __maxnreg__(tb2d::Cfg<K>::MAXREG)
     k_tb2d_cycle(const __grid_constant__ CUtensorMap tm_x0,
                  const __grid_constant__ CUtensorMap tm_x1,
                  const __grid_constant__ CUtensorMap tm_b, TbArgs a) {
     using C = tb2d::Cfg<K>;
-    constexpr int S = C::S;
     using L = TbLayout<K>;
+    constexpr int S = C::S;
     __shared__ double sh[32 * S];
     __shared__ double red[S];
     __shared__ double sh1[32];
-    for (int i = threadIdx.x; i < 2 * C::EX; i += blockDim.x) L::e(0)[i] = 0.0;
+    // zero halo rows (the rows beyond the first and last warp are never written)
+    for (int i = threadIdx.x; i < 2 * C::HBUF; i += blockDim.x) L::top(0)[i] = 0.0;
     if (threadIdx.x == 0) {
-        mbar_init(L::bar(0), 1);
-        mbar_init(L::bar(1), 1);
+        mbar_init(L::bar(), 1);
         prefetch_tensormap(&tm_x0);
         prefetch_tensormap(&tm_x1);
         prefetch_tensormap(&tm_b);
     }
     __syncthreads();
-    // owned-point bits of this thread's column segment (tile-independent)
+    // owned-point bits of this thread's CW x V block (tile-independent)
     unsigned ownmask = 0u;
     {
-        const int c = threadIdx.x % C::RX, r0 = (threadIdx.x / C::RX) * C::V;
-        if (c >= S && c < S + C::TX) {
+        const int c0 = (threadIdx.x & 31) * C::CW, r0 = (threadIdx.x >> 5) * C::V;
 #pragma unroll
-            for (int v = 0; v < C::V; ++v)
-                if (r0 + v >= S && r0 + v < S + C::TY) ownmask |= 1u << v;
-        }
+        for (int v = 0; v < C::V; ++v)
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j)
+                if (c0 + j >= S && c0 + j < S + C::TX && r0 + v >= S && r0 + v < S + C::TY)
+                    ownmask |= 1u << (v * C::CW + j);
     }
     uint32_t phase = 0;
-    int slot = 0;
     const int nb = gridDim.x;
     double* const buf[2] = {a.buf0, a.buf1};
     const CUtensorMap* const tmx[2] = {&tm_x0, &tm_x1};
@@ -300,7 +354,7 @@ __global__ void __maxnreg__(tb2d::Cfg<K>::MAXREG)
 #pragma unroll
         for (int t = 0; t < S; ++t) acc[t] = 0.0;
         tb2d_pass<K>(a, tmx[p & 1], &tm_b, buf[(p + 1) & 1], k0, h, acc, true, ownmask, phase,
-                     slot, issued);
+                     issued);
         issued = false;
         double* part = a.partials + (size_t)(p & 1) * kTbMaxSub * nb;
         block_sums<S>(acc, h, sh, red);
@@ -308,8 +362,7 @@ __global__ void __maxnreg__(tb2d::Cfg<K>::MAXREG)
         grid_barrier();
         // Speculatively start the next pass's first tile while the stop test runs.
         if (p + 1 < npasses && (int)blockIdx.x < a.ntiles) {
-            if (threadIdx.x == 0)
-                tb2d_issue<K>(a, tmx[(p + 1) & 1], &tm_b, blockIdx.x, slot);
+            if (threadIdx.x == 0) tb2d_issue<K>(a, tmx[(p + 1) & 1], &tm_b, blockIdx.x);
             issued = true;
         }
         reduce_partials_multi(part, nb, h, red);
@@ -328,8 +381,8 @@ __global__ void __maxnreg__(tb2d::Cfg<K>::MAXREG)
             stopped = true;
             executed = k0 + stop_t;
             if (issued) {  // drain the speculative load
-                mbar_wait(L::bar(slot), (phase >> slot) & 1u);
-                phase ^= 1u << slot;
+                mbar_wait(L::bar(), phase);
+                phase ^= 1u;
                 issued = false;
                 __syncthreads();
             }
@@ -338,7 +391,7 @@ __global__ void __maxnreg__(tb2d::Cfg<K>::MAXREG)
             } else {
                 // rollback: x_{k0+stop_t} from the intact pass input
                 tb2d_pass<K>(a, tmx[p & 1], &tm_b, buf[(p + 1) & 1], k0, stop_t, acc, false,
-                             ownmask, phase, slot, false);
+                             ownmask, phase, false);
                 grid_barrier();
                 result = (p + 1) & 1;
             }
@@ -403,8 +456,8 @@ cudaError_t tb_plan_init(TbPlan& plan, const Geom& g, int num_sms) {
     plan_tiles<0>(plan, g, num_sms);
     plan_tiles<1>(plan, g, num_sms);
     // variant: SRJ_TB_VARIANT=0|1 overrides the default (tuning only)
-    plan.small_variant = 1;
-    if (const char* v = getenv("SRJ_TB_VARIANT")) plan.small_variant = atoi(v) == 0 ? 0 : 1;
+    plan.small_variant = 0;
+    if (const char* v = getenv("SRJ_TB_VARIANT")) plan.small_variant = atoi(v) == 1 ? 1 : 0;
     plan.supported = true;
     return cudaSuccess;
 }
@@ -445,8 +498,8 @@ cudaError_t tb_launch_cycle(const TbPlan& plan, const Geom& g, double* x, double
     a.hist = hist;
     a.out_i = out_i;
     a.out_d = out_d;
-    if (plan.small_variant == 0) return launch_variant<0>(plan, g, a, x, x_alt, b, st);
-    return launch_variant<1>(plan, g, a, x, x_alt, b, st);
+    if (plan.small_variant == 1) return launch_variant<1>(plan, g, a, x, x_alt, b, st);
+    return launch_variant<0>(plan, g, a, x, x_alt, b, st);
 }
 
 }  // namespace srj
