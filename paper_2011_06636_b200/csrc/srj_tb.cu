@@ -70,8 +70,8 @@ struct CfgBase {
     static constexpr int STAGE = RX * RY;          // doubles per staged box
     static constexpr int HROWS = NSEG + 2;         // halo rows incl. a zero row each side
     static constexpr int HBUF = 2 * HROWS * RX;    // top + bottom rows, one parity
-    // x stage, b stage, halo rows [2 parities], one mbarrier
-    static constexpr size_t SMEM = (size_t)(2 * STAGE + 2 * HBUF) * sizeof(double) + 16;
+    // x stage, b stage, halo rows [2 parities], TMA + 2 halo mbarriers
+    static constexpr size_t SMEM = (size_t)(2 * STAGE + 2 * HBUF) * sizeof(double) + 32;
     static constexpr uint32_t TX_BYTES = 2u * STAGE * sizeof(double);
 };
 
@@ -81,7 +81,10 @@ struct Cfg;
 template <>
 struct Cfg<0> : CfgBase<4, 2, 6, 12> {};  // 64x72 region, 56x64 tile, 384 threads
 template <>
-struct Cfg<1> : CfgBase<4, 4, 6, 12> {};  // 128x72 region, 120x64 tile, 384 threads
+struct Cfg<1> : CfgBase<4, 2, 9, 8> {};   // 64x72 region, 56x64 tile, 256 threads
+// Measured on B200 (2048^2 / 4096^2, us per sweep): K=0 9.4 / 33.5, K=1
+// 10.2 / 36.7; 16-warp 64x96 and 18-warp 64x72 shapes spill (10.9 / 38.4),
+// 64x128 spills heavily (15.7), 4 columns per lane (128x72) spills (15.0).
 constexpr int kVariants = 2;
 
 }  // namespace tb2d
@@ -120,6 +123,10 @@ struct TbLayout {
     __device__ static __forceinline__ uint64_t* bar() {
         return reinterpret_cast<uint64_t*>(tb_smem + BAR);
     }
+    // halo hand-off barriers [2] (one arrival per warp)
+    __device__ static __forceinline__ uint64_t* hbar(int i) {
+        return reinterpret_cast<uint64_t*>(tb_smem + BAR) + 1 + i;
+    }
 };
 
 // CW contiguous doubles at a 16-byte aligned shared address.
@@ -151,6 +158,14 @@ __device__ __forceinline__ void tb2d_issue(const TbArgs& a, const CUtensorMap* t
     tma_load_2d(L::stb(), tm_b, ox - S, oy - S, L::bar());
 }
 
+// acc += r*r when cond != 0, as one predicated DFMA (a C++ conditional
+// becomes a DFMA plus two FSELs).
+__device__ __forceinline__ void fma_sq_if(double& acc, double r, unsigned cond) {
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p fma.rn.f64 %0, %1, %1, %0;\n\t}"
+        : "+d"(acc)
+        : "d"(r), "r"(cond));
+}
+
 template <int K>
 struct TileRegs {
     using C = tb2d::Cfg<K>;
@@ -160,47 +175,97 @@ struct TileRegs {
 // H sub-sweeps (compile-time, H <= S) of the tile held in registers.  MASKED
 // tiles reach outside the grid: points there (bit clear in `inmask`, bit
 // v*CW+j) are held at 0.  Points with a bit set in `accmask` add r^2 to acc[t].
+//
+// Halo hand-off between sub-sweeps is a split barrier: after publishing its
+// edge rows a warp arrives on mbarrier `na & 1` (one elected lane per warp),
+// computes its interior rows -- which need no halo -- and only then waits for
+// the other warps' arrivals before its two edge rows.  `na` counts arrival
+// rounds (identical in every thread).
 template <int K, int H, bool MASKED>
 __device__ __forceinline__ void tile_sweeps(TileRegs<K>& R, const double* omegas, const Geom& g,
                                             int warp, int lane, unsigned inmask, unsigned accmask,
-                                            double (&acc)[tb2d::Cfg<K>::S]) {
+                                            double (&acc)[tb2d::Cfg<K>::S], uint32_t& na) {
     using C = tb2d::Cfg<K>;
     using L = TbLayout<K>;
     constexpr int V = C::V, CW = C::CW, RX = C::RX;
+    static_assert(V >= 3 && CW == 2, "row-pair groups of a 2-column lane");
     const double coff = g.c_off, cdiag = g.c_diag, inv = g.inv_diag;
     const int col = lane * CW;
 #pragma unroll
     for (int t = 0; t < H; ++t) {
         const double w = __ldg(omegas + t);
-        double hs[CW], hn[CW];  // p of the rows above / below this warp's rows
-        lds_cols<CW>(hs, L::bot(t) + warp * RX + col);        // bottom row of warp-1
-        lds_cols<CW>(hn, L::top(t) + (warp + 2) * RX + col);  // top row of warp+1
         double pw[V], pe[V];  // p across the lane boundary
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             pw[v] = __shfl_up_sync(0xffffffffu, R.p[v][CW - 1], 1);
             pe[v] = __shfl_down_sync(0xffffffffu, R.p[v][0], 1);
         }
+        double hs[CW], hn[CW];  // p of the rows above / below this warp's rows
+        double sq[4] = {0.0, 0.0, 0.0, 0.0};  // r^2 partial sums, one per group slot
+        // Rows va and vb (vb < 0: va only), both columns, computed in lockstep
+        // so the independent dependency chains interleave (fp64 latency ~9
+        // clk on B200).  Neighbours are the OLD p (updated after all rows).
+        auto group = [&](int va, int vb) {
+            constexpr int NP = 4;
+            const int np = vb >= 0 ? 4 : 2;
+            double y[NP], rr[NP];
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
+            for (int k = 0; k < NP; ++k) {
+                if (k >= np) break;
+                const int v = k < 2 ? va : vb, j = k & 1;
+                y[k] = DADD(0.0, v == 0 ? hs[j] : R.p[v - 1][j]);
+            }
 #pragma unroll
-            for (int j = 0; j < CW; ++j) {
-                const double ps = v == 0 ? hs[j] : R.p[v - 1][j];
-                const double pwv = j == 0 ? pw[v] : R.p[v][j - 1];
-                const double pev = j == CW - 1 ? pe[v] : R.p[v][j + 1];
-                const double pn = v == V - 1 ? hn[j] : R.p[v + 1][j];
-                double y = DADD(0.0, ps);
-                y = DADD(y, pwv);
-                y = DADD(y, DMUL(cdiag, R.x[v][j]));
-                y = DADD(y, pev);
-                y = DADD(y, pn);
-                const double rr = DSUB(R.b[v][j], y);
-                const double xn = relax(R.x[v][j], inv, rr, w);
+            for (int k = 0; k < NP; ++k) {
+                if (k >= np) break;
+                const int v = k < 2 ? va : vb, j = k & 1;
+                y[k] = DADD(y[k], j == 0 ? pw[v] : R.p[v][j - 1]);
+            }
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                if (k >= np) break;
+                const int v = k < 2 ? va : vb, j = k & 1;
+                y[k] = DADD(y[k], DMUL(cdiag, R.x[v][j]));
+            }
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                if (k >= np) break;
+                const int v = k < 2 ? va : vb, j = k & 1;
+                y[k] = DADD(y[k], j == CW - 1 ? pe[v] : R.p[v][j + 1]);
+            }
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                if (k >= np) break;
+                const int v = k < 2 ? va : vb, j = k & 1;
+                y[k] = DADD(y[k], v == V - 1 ? hn[j] : R.p[v + 1][j]);
+            }
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                if (k >= np) break;
+                const int v = k < 2 ? va : vb, j = k & 1;
+                rr[k] = DSUB(R.b[v][j], y[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                if (k >= np) break;
+                const int v = k < 2 ? va : vb, j = k & 1;
                 const int bit = v * CW + j;
-                if ((accmask >> bit) & 1u) acc[t] = fma(rr, rr, acc[t]);
+                const double xn = relax(R.x[v][j], inv, rr[k], w);
+                fma_sq_if(sq[k], rr[k], (accmask >> bit) & 1u);
                 R.x[v][j] = (!MASKED || ((inmask >> bit) & 1u)) ? xn : 0.0;
             }
+        };
+#pragma unroll
+        for (int v = 1; v + 1 < V - 1; v += 2) group(v, v + 1);
+        if ((V - 2) & 1) group(V - 2, -1);
+        if (t > 0) {  // halos of sub-sweep t were published by every warp
+            mbar_wait(L::hbar(na & 1), (na >> 1) & 1);
+            ++na;
         }
+        lds_cols<CW>(hs, L::bot(t) + warp * RX + col);        // bottom row of warp-1
+        lds_cols<CW>(hn, L::top(t) + (warp + 2) * RX + col);  // top row of warp+1
+        group(0, V - 1);
+        acc[t] = DADD(acc[t], DADD(DADD(sq[0], sq[1]), DADD(sq[2], sq[3])));
 #pragma unroll
         for (int v = 0; v < V; ++v)
 #pragma unroll
@@ -208,7 +273,8 @@ __device__ __forceinline__ void tile_sweeps(TileRegs<K>& R, const double* omegas
         if (t + 1 < H) {
             sts_cols<CW>(L::top(t + 1) + (warp + 1) * RX + col, R.p[0]);
             sts_cols<CW>(L::bot(t + 1) + (warp + 1) * RX + col, R.p[V - 1]);
-            __syncthreads();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(L::hbar(na & 1));
         }
     }
 }
@@ -216,12 +282,13 @@ __device__ __forceinline__ void tile_sweeps(TileRegs<K>& R, const double* omegas
 template <int K, bool MASKED>
 __device__ __forceinline__ void tile_dispatch(int h, TileRegs<K>& R, const double* omegas,
                                               const Geom& g, int warp, int lane, unsigned inmask,
-                                              unsigned accmask, double (&acc)[tb2d::Cfg<K>::S]) {
+                                              unsigned accmask, double (&acc)[tb2d::Cfg<K>::S],
+                                              uint32_t& na) {
     constexpr int S = tb2d::Cfg<K>::S;
 #define SRJ_TB_CASE(H)                                                                      \
     case H:                                                                                 \
         if constexpr (H <= S)                                                               \
-            tile_sweeps<K, H, MASKED>(R, omegas, g, warp, lane, inmask, accmask, acc);      \
+            tile_sweeps<K, H, MASKED>(R, omegas, g, warp, lane, inmask, accmask, acc, na);  \
         break;
     switch (h) {
         SRJ_TB_CASE(1)
@@ -240,7 +307,7 @@ __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm
                                           const CUtensorMap* tm_b, double* __restrict__ xout,
                                           int k0, int h, double (&acc)[tb2d::Cfg<K>::S],
                                           bool accumulate, unsigned ownmask, uint32_t& phase,
-                                          bool first_issued) {
+                                          bool first_issued, uint32_t& na) {
     using C = tb2d::Cfg<K>;
     using L = TbLayout<K>;
     constexpr int S = C::S, V = C::V, CW = C::CW, RX = C::RX;
@@ -283,9 +350,9 @@ __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm
         if (threadIdx.x == 0 && q + (int)gridDim.x < a.ntiles)
             tb2d_issue<K>(a, tm_in, tm_b, q + gridDim.x);
         if (masked)
-            tile_dispatch<K, true>(h, R, a.omegas + k0, a.g, warp, lane, inmask, accmask, acc);
+            tile_dispatch<K, true>(h, R, a.omegas + k0, a.g, warp, lane, inmask, accmask, acc, na);
         else
-            tile_dispatch<K, false>(h, R, a.omegas + k0, a.g, warp, lane, inmask, accmask, acc);
+            tile_dispatch<K, false>(h, R, a.omegas + k0, a.g, warp, lane, inmask, accmask, acc, na);
         if (storemask) {
 #pragma unroll
             for (int v = 0; v < V; ++v) {
@@ -323,6 +390,8 @@ __global__ void __launch_bounds__(tb2d::Cfg<K>::THREADS, 1) __maxnreg__(tb2d::Cf
     for (int i = threadIdx.x; i < 2 * C::HBUF; i += blockDim.x) L::top(0)[i] = 0.0;
     if (threadIdx.x == 0) {
         mbar_init(L::bar(), 1);
+        mbar_init(L::hbar(0), C::NSEG);
+        mbar_init(L::hbar(1), C::NSEG);
         prefetch_tensormap(&tm_x0);
         prefetch_tensormap(&tm_x1);
         prefetch_tensormap(&tm_b);
@@ -339,7 +408,7 @@ __global__ void __launch_bounds__(tb2d::Cfg<K>::THREADS, 1) __maxnreg__(tb2d::Cf
                 if (c0 + j >= S && c0 + j < S + C::TX && r0 + v >= S && r0 + v < S + C::TY)
                     ownmask |= 1u << (v * C::CW + j);
     }
-    uint32_t phase = 0;
+    uint32_t phase = 0, na = 0;
     const int nb = gridDim.x;
     double* const buf[2] = {a.buf0, a.buf1};
     const CUtensorMap* const tmx[2] = {&tm_x0, &tm_x1};
@@ -354,7 +423,7 @@ __global__ void __launch_bounds__(tb2d::Cfg<K>::THREADS, 1) __maxnreg__(tb2d::Cf
 #pragma unroll
         for (int t = 0; t < S; ++t) acc[t] = 0.0;
         tb2d_pass<K>(a, tmx[p & 1], &tm_b, buf[(p + 1) & 1], k0, h, acc, true, ownmask, phase,
-                     issued);
+                     issued, na);
         issued = false;
         double* part = a.partials + (size_t)(p & 1) * kTbMaxSub * nb;
         block_sums<S>(acc, h, sh, red);
@@ -391,7 +460,7 @@ __global__ void __launch_bounds__(tb2d::Cfg<K>::THREADS, 1) __maxnreg__(tb2d::Cf
             } else {
                 // rollback: x_{k0+stop_t} from the intact pass input
                 tb2d_pass<K>(a, tmx[p & 1], &tm_b, buf[(p + 1) & 1], k0, stop_t, acc, false,
-                             ownmask, phase, false);
+                             ownmask, phase, false, na);
                 grid_barrier();
                 result = (p + 1) & 1;
             }
@@ -447,17 +516,20 @@ cudaError_t tb_plan_init(TbPlan& plan, const Geom& g, int num_sms) {
     plan = TbPlan();
     // TMA needs 16-byte row pitch: even nx.
     if (g.fam != F2D || (g.nx & 1) || !tma_available()) return cudaSuccess;
-    int occ[tb2d::kVariants] = {0, 0};
+    int occ[tb2d::kVariants] = {};
     cudaError_t e;
     if ((e = setup_variant<0>(occ[0])) != cudaSuccess) return e;
     if ((e = setup_variant<1>(occ[1])) != cudaSuccess) return e;
-    plan.occupancy = std::min(occ[0], occ[1]);
+    // variant: SRJ_TB_VARIANT=k overrides the default (tuning only)
+    plan.small_variant = 0;
+    if (const char* v = getenv("SRJ_TB_VARIANT")) {
+        const int k = atoi(v);
+        if (k >= 0 && k < tb2d::kVariants) plan.small_variant = k;
+    }
+    plan.occupancy = occ[plan.small_variant];
     if (plan.occupancy < 1) return cudaSuccess;
     plan_tiles<0>(plan, g, num_sms);
     plan_tiles<1>(plan, g, num_sms);
-    // variant: SRJ_TB_VARIANT=0|1 overrides the default (tuning only)
-    plan.small_variant = 0;
-    if (const char* v = getenv("SRJ_TB_VARIANT")) plan.small_variant = atoi(v) == 1 ? 1 : 0;
     plan.supported = true;
     return cudaSuccess;
 }
@@ -498,8 +570,10 @@ cudaError_t tb_launch_cycle(const TbPlan& plan, const Geom& g, double* x, double
     a.hist = hist;
     a.out_i = out_i;
     a.out_d = out_d;
-    if (plan.small_variant == 1) return launch_variant<1>(plan, g, a, x, x_alt, b, st);
-    return launch_variant<0>(plan, g, a, x, x_alt, b, st);
+    switch (plan.small_variant) {
+        case 1: return launch_variant<1>(plan, g, a, x, x_alt, b, st);
+        default: return launch_variant<0>(plan, g, a, x, x_alt, b, st);
+    }
 }
 
 }  // namespace srj

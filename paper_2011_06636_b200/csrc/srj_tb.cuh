@@ -13,9 +13,9 @@ constexpr int kTbMaxSub = 8;  // most sweeps fused into one pass
 struct TbPlan {
     bool supported = false;
     // per kernel variant (see srj_tb.cu, tb2d::Cfg<K>)
-    int blocks[4] = {0, 0, 0, 0};   // cooperative grid (one CTA per SM)
-    int tiles_x[4] = {0, 0, 0, 0};
-    int ntiles[4] = {0, 0, 0, 0};
+    int blocks[8] = {};   // cooperative grid (one CTA per SM)
+    int tiles_x[8] = {};
+    int ntiles[8] = {};
     int small_variant = 1;          // variant launched (tb2d::Cfg<K>)
     int occupancy = 0;              // min resident CTAs per SM over the variants
 };
