@@ -64,7 +64,8 @@ class OpInfo(ctypes.Structure):
                1: "srj::k_tb2d_cycle (TMA temporal blocking)",
                2: "srj::k_cycle2d (TMA tile streaming)",
                3: "srj::k_cycle3d (TMA plane ring)",
-               4: "srj::k_ws2d_cycle (warp-streaming temporal blocking)"}
+               4: "srj::k_ws2d_cycle (warp-streaming temporal blocking)",
+               5: "srj::k_tb3d_cycle (TMA z-wavefront temporal blocking)"}
 
     def as_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}

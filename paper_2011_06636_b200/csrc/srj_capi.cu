@@ -220,6 +220,7 @@ struct srj_op {
     double* h_out_d = nullptr;
     double* h_hist = nullptr;
     TbPlan tb;                   // temporal-blocking plan (srj_tb.cuh)
+    Tb3Plan tb3;                 // 3D temporal-blocking plan (srj_tb3d.cu)
     Plan3D p3;                   // plane-streaming 3D plan (srj_3d.cuh)
     Plan2D p2;                   // tile-streaming 2D plan (srj_2d.cuh)
     WsPlan ws;                   // warp-streaming temporal blocking (srj_ws2d.cuh)
@@ -366,8 +367,14 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("temporal-blocking setup failed: ") + cudaGetErrorString(e));
     }
-    // Default: 4 sweeps per pass where a temporally blocked kernel exists
-    // (measured best on B200 for 2D), else one per pass.
+    if ((e = tb3_plan_init(op->tb3, g, op->num_sms)) != cudaSuccess) {
+        srj_op_destroy(op);
+        return fail(SRJ_CUDA_ERROR, std::string("3D temporal-blocking setup failed: ") + cudaGetErrorString(e));
+    }
+    // Default: 4 fused sweeps per pass where the 2D temporally blocked kernel
+    // exists, else one per pass.  3D keeps the HBM-bound plane ring by default:
+    // the z-wavefront TB kernel (sweeps_per_pass 2) measured slower on B200
+    // (DESIGN.md §4).
     op->sweeps_per_pass = (op->tb.supported || op->ws.supported) ? 4 : 1;
     op->slot_capacity = std::max(op->p3.slots, kApplyBlocksPerSm * op->num_sms);
     for (int s = 0; s < kSlots; ++s) {
@@ -432,11 +439,12 @@ int srj_op_describe(const srj_op* op, srj_op_info* info) {
     info->cycle_blocks = op->coop_blocks;
     info->cycle_threads = op->coop_threads;
     info->sweeps_per_pass = op->sweeps_per_pass;
-    info->tb_supported = op->tb.supported ? 1 : 0;
-    info->tb_blocks = op->tb.blocks[op->tb.small_variant];
-    info->tb_occupancy = op->tb.occupancy;
-    info->tb_tiles = op->tb.ntiles[op->tb.small_variant];
-    info->cycle_kernel = op->p3.supported                                 ? SRJ_KERNEL_PLANE3D
+    info->tb_supported = (op->tb.supported || op->tb3.supported) ? 1 : 0;
+    info->tb_blocks = op->tb3.supported ? op->tb3.blocks : op->tb.blocks[op->tb.small_variant];
+    info->tb_occupancy = op->tb3.supported ? 1 : op->tb.occupancy;
+    info->tb_tiles = op->tb3.supported ? op->tb3.ntiles : op->tb.ntiles[op->tb.small_variant];
+    info->cycle_kernel = (op->sweeps_per_pass > 1 && op->tb3.supported)  ? SRJ_KERNEL_TB3D
+                         : op->p3.supported                               ? SRJ_KERNEL_PLANE3D
                          : (op->sweeps_per_pass > 1 && op->ws.supported &&
                             op->tb_kind == SRJ_TB_WARP_STREAM) ? SRJ_KERNEL_WS2D
                          : (op->sweeps_per_pass > 1 && op->tb.supported) ? SRJ_KERNEL_TB2D
@@ -517,7 +525,11 @@ int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
     const int Meff = (int)std::min<int64_t>(M, std::max<int64_t>(budget, 0));
     if (Meff == 0) return SRJ_OK;
 
-    if (op->p3.supported) {
+    if (op->sweeps_per_pass > 1 && op->tb3.supported) {
+        CUDA_TRY(tb3_launch_cycle(op->tb3, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,
+                                  op->partials, op->hist, op->out_i, op->out_d, st));
+        out->launches = 1;
+    } else if (op->p3.supported) {
         CUDA_TRY(launch3d_cycle(op->p3, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,
                                 op->partials, op->hist, op->out_i, op->out_d, st));
         out->launches = 1;

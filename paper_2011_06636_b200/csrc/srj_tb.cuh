@@ -33,4 +33,21 @@ cudaError_t tb_launch_cycle(const TbPlan& plan, const Geom& g, double* x, double
                             double baseline, double* partials, double* hist, int* out_i,
                             double* out_d, cudaStream_t st);
 
+// 3D 7-point temporal blocking (srj_tb3d.cu): S = sweeps fused per pass.
+struct Tb3Plan {
+    bool supported = false;
+    int blocks = 0, tiles_x = 0, ntiles = 0;
+    int sweeps = 0;
+    int variant = 0;  // tb3d::C<variant> (SRJ_TB3_VARIANT, tuning only)
+};
+
+cudaError_t tb3_plan_init(Tb3Plan& plan, const Geom& g, int num_sms);
+
+// One cycle of M sweeps, plan.sweeps per pass; outputs as tb_launch_cycle.
+// x, x_alt and b must have zero ghost planes (Dirichlet).
+cudaError_t tb3_launch_cycle(const Tb3Plan& plan, const Geom& g, double* x, double* x_alt,
+                             const double* b, const double* omegas, int M, double tol,
+                             double baseline, double* partials, double* hist, int* out_i,
+                             double* out_d, cudaStream_t st);
+
 }  // namespace srj
