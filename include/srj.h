@@ -141,8 +141,9 @@ enum srj_cycle_kernel {
     SRJ_KERNEL_TILE2D = 2,     /* TMA tile streaming 2D (constant / variable)   */
     SRJ_KERNEL_PLANE3D = 3,    /* TMA plane streaming 3D                        */
     SRJ_KERNEL_WS2D = 4,       /* warp-streaming temporal blocking 2D           */
-    SRJ_KERNEL_TB3D = 5        /* temporally blocked 3D z-wavefront (2 sweeps
+    SRJ_KERNEL_TB3D = 5,       /* temporally blocked 3D z-wavefront (2 sweeps
                                   per pass when sweeps_per_pass > 1)            */
+    SRJ_KERNEL_TBVAR = 6       /* temporally blocked 2D variable coefficient    */
 };
 
 /* Temporally blocked 2D kernel used when sweeps_per_pass > 1. */

@@ -65,7 +65,8 @@ class OpInfo(ctypes.Structure):
                2: "srj::k_cycle2d (TMA tile streaming)",
                3: "srj::k_cycle3d (TMA plane ring)",
                4: "srj::k_ws2d_cycle (warp-streaming temporal blocking)",
-               5: "srj::k_tb3d_cycle (TMA z-wavefront temporal blocking)"}
+               5: "srj::k_tb3d_cycle (TMA z-wavefront temporal blocking)",
+               6: "srj::k_tbvar_cycle (TMA var-coef temporal blocking)"}
 
     def as_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}

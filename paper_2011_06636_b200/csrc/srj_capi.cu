@@ -221,6 +221,7 @@ struct srj_op {
     double* h_hist = nullptr;
     TbPlan tb;                   // temporal-blocking plan (srj_tb.cuh)
     Tb3Plan tb3;                 // 3D temporal-blocking plan (srj_tb3d.cu)
+    TbvPlan tbv;                 // var-coef 2D temporal-blocking plan (srj_tbvar.cu)
     Plan3D p3;                   // plane-streaming 3D plan (srj_3d.cuh)
     Plan2D p2;                   // tile-streaming 2D plan (srj_2d.cuh)
     WsPlan ws;                   // warp-streaming temporal blocking (srj_ws2d.cuh)
@@ -367,6 +368,10 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("temporal-blocking setup failed: ") + cudaGetErrorString(e));
     }
+    if ((e = tbv_plan_init(op->tbv, g, op->num_sms)) != cudaSuccess) {
+        srj_op_destroy(op);
+        return fail(SRJ_CUDA_ERROR, std::string("var-coef temporal-blocking setup failed: ") + cudaGetErrorString(e));
+    }
     if ((e = tb3_plan_init(op->tb3, g, op->num_sms)) != cudaSuccess) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("3D temporal-blocking setup failed: ") + cudaGetErrorString(e));
@@ -375,7 +380,7 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
     // exists, else one per pass.  3D keeps the HBM-bound plane ring by default:
     // the z-wavefront TB kernel (sweeps_per_pass 2) measured slower on B200
     // (DESIGN.md §4).
-    op->sweeps_per_pass = (op->tb.supported || op->ws.supported) ? 4 : 1;
+    op->sweeps_per_pass = (op->tb.supported || op->ws.supported || op->tbv.supported) ? 4 : 1;
     op->slot_capacity = std::max(op->p3.slots, kApplyBlocksPerSm * op->num_sms);
     for (int s = 0; s < kSlots; ++s) {
         if ((e = cudaMalloc(&op->slot_part[s], op->slot_capacity * sizeof(double))) != cudaSuccess) {
@@ -439,11 +444,14 @@ int srj_op_describe(const srj_op* op, srj_op_info* info) {
     info->cycle_blocks = op->coop_blocks;
     info->cycle_threads = op->coop_threads;
     info->sweeps_per_pass = op->sweeps_per_pass;
-    info->tb_supported = (op->tb.supported || op->tb3.supported) ? 1 : 0;
-    info->tb_blocks = op->tb3.supported ? op->tb3.blocks : op->tb.blocks[op->tb.small_variant];
-    info->tb_occupancy = op->tb3.supported ? 1 : op->tb.occupancy;
-    info->tb_tiles = op->tb3.supported ? op->tb3.ntiles : op->tb.ntiles[op->tb.small_variant];
-    info->cycle_kernel = (op->sweeps_per_pass > 1 && op->tb3.supported)  ? SRJ_KERNEL_TB3D
+    info->tb_supported = (op->tb.supported || op->tb3.supported || op->tbv.supported) ? 1 : 0;
+    info->tb_blocks = op->tbv.supported ? op->tbv.blocks
+                      : op->tb3.supported ? op->tb3.blocks : op->tb.blocks[op->tb.small_variant];
+    info->tb_occupancy = (op->tbv.supported || op->tb3.supported) ? 1 : op->tb.occupancy;
+    info->tb_tiles = op->tbv.supported ? op->tbv.ntiles
+                     : op->tb3.supported ? op->tb3.ntiles : op->tb.ntiles[op->tb.small_variant];
+    info->cycle_kernel = (op->sweeps_per_pass > 1 && op->tbv.supported)  ? SRJ_KERNEL_TBVAR
+                         : (op->sweeps_per_pass > 1 && op->tb3.supported) ? SRJ_KERNEL_TB3D
                          : op->p3.supported                               ? SRJ_KERNEL_PLANE3D
                          : (op->sweeps_per_pass > 1 && op->ws.supported &&
                             op->tb_kind == SRJ_TB_WARP_STREAM) ? SRJ_KERNEL_WS2D
@@ -525,7 +533,12 @@ int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
     const int Meff = (int)std::min<int64_t>(M, std::max<int64_t>(budget, 0));
     if (Meff == 0) return SRJ_OK;
 
-    if (op->sweeps_per_pass > 1 && op->tb3.supported) {
+    if (op->sweeps_per_pass > 1 && op->tbv.supported) {
+        CUDA_TRY(tbv_launch_cycle(op->tbv, op->g, x, x_alt, b, omegas_dev, Meff,
+                                  op->sweeps_per_pass, tol, baseline, op->partials, op->hist,
+                                  op->out_i, op->out_d, st));
+        out->launches = 1;
+    } else if (op->sweeps_per_pass > 1 && op->tb3.supported) {
         CUDA_TRY(tb3_launch_cycle(op->tb3, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,
                                   op->partials, op->hist, op->out_i, op->out_d, st));
         out->launches = 1;

@@ -50,4 +50,20 @@ cudaError_t tb3_launch_cycle(const Tb3Plan& plan, const Geom& g, double* x, doub
                              double baseline, double* partials, double* hist, int* out_i,
                              double* out_d, cudaStream_t st);
 
+// 2D variable-coefficient temporal blocking (srj_tbvar.cu), 4 sweeps per pass.
+struct TbvPlan {
+    bool supported = false;
+    int blocks = 0, tiles_x = 0, ntiles = 0;
+    double* fx_pad = nullptr;  // fx with a 16-byte row pitch (nx + 2)
+    int fx_pitch = 0;
+    double* inv = nullptr;     // 1 / diagonal, precomputed (reference order)
+};
+
+cudaError_t tbv_plan_init(TbvPlan& plan, const Geom& g, int num_sms);
+void tbv_plan_free(TbvPlan& plan);
+cudaError_t tbv_launch_cycle(const TbvPlan& plan, const Geom& g, double* x, double* x_alt,
+                             const double* b, const double* omegas, int M, int s, double tol,
+                             double baseline, double* partials, double* hist, int* out_i,
+                             double* out_d, cudaStream_t st);
+
 }  // namespace srj
