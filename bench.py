@@ -9,8 +9,9 @@ until the relative residual <= 1e-8.  One step = one full solve.
   e2e       the same metric through the public API `solve()` with pinned host
             b/x0 in and x out (H2D + D2H inside the timed region)
   roofline  algorithmic bytes of the cycle kernel (24 B per point-sweep + 16 B
-            per point for the end-of-cycle residual) / its event-timed duration
-            vs the measured HBM copy bandwidth (MEASURED_PEAKS.json)
+            per point for the end-of-cycle residual; 40 B + 32 B var-coef) / its
+            event-timed duration vs the measured HBM copy bandwidth
+            (MEASURED_PEAKS.json)
   cpu_baseline  the oracle port (oracle/srj_oracle.c, OpenMP) on a bounded
             sample of the same workload on this host's cores
 
@@ -41,6 +42,8 @@ CONFIG_DESC = {
     "c5": "3D Poisson 7-pt 1024x1024x(128N) z-slabs over N GPUs, 50 heuristic cycles",
 }
 BYTES_PER_UPDATE = {"1d3": 24, "2d5": 24, "3d7": 24, "2d5var": 40}
+# end-of-cycle residual pass: reads x and b (+ both face arrays, var-coef)
+RESIDUAL_BYTES = {"1d3": 16, "2d5": 16, "3d7": 16, "2d5var": 32}
 L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
 
 
@@ -261,6 +264,42 @@ def run_slabs(args, rank, world, local):
         total_ms = float(t.item())
     n_global = int(np.prod(shape))
     value = n_global * sum(sweeps) / (total_ms * 1e-3) / 1e9
+
+    # e2e: each rank stages its slab's b and x0 from pinned host memory and reads
+    # its slab of the solution back (H2D + D2H inside the timed region)
+    s0 = slabs[0]
+    solver.load(seed=args.seed)
+    b_host = torch.empty(s0.A.n, dtype=torch.float64, pin_memory=True)
+    b_host.copy_(s0.b.interior)
+    x0_host = torch.zeros(s0.A.n, dtype=torch.float64, pin_memory=True)
+    x_out = torch.empty(s0.A.n, dtype=torch.float64, pin_memory=True)
+
+    def one_e2e():
+        s0.b.copy_(b_host)
+        s0.x.buf.zero_()
+        s0.x_alt.buf.zero_()
+        s0.x.copy_(x0_host)
+        r = solver.solve(ctrl, rule, record_history=False, max_cycles=args.cycles)
+        x_out.copy_(r.x[0])
+        return r
+
+    one_e2e()  # untimed warm-up
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e2e_ms, e2e_sweeps = [], []
+    for _ in range(max(1, min(args.steps, 2))):
+        t0 = time.perf_counter()
+        r = one_e2e()
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e_sweeps.append(r.total_iterations)
+    e2e_total = sum(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_val = n_global * sum(e2e_sweeps) / (e2e_total * 1e-3) / 1e9
     per_gpu_bytes = 24.0 * slabs[0].A.n * sum(sweeps)
     peak, peak_kind = measured_peak()
     achieved = per_gpu_bytes / (total_ms * 1e-3) / 1e9
@@ -279,6 +318,9 @@ def run_slabs(args, rank, world, local):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
                      "kernel": "srj::k_sweep3d (slab sweep, whole step incl. exchange)"},
+        "e2e": {"value": e2e_val, "unit": "GLUP/s", "h2d_bytes_per_step": 16 * s0.A.n * world,
+                "d2h_bytes_per_step": 8 * s0.A.n * world,
+                "ms_per_step": e2e_total / len(e2e_ms)},
         "clocks": clocks.summary(),
         "gpu_launches": int(sum(sweeps) * 3 + len(rep.cycles) * 2),
     }
@@ -342,7 +384,7 @@ def run_ours(args, rank, world, local):
         e1.synchronize()
         if out.executed > 0:
             launch_ms.append(e0.elapsed_time(e1))
-            launch_bytes.append(bpu * A.n * out.executed + 16 * A.n)
+            launch_bytes.append(bpu * A.n * out.executed + RESIDUAL_BYTES[family] * A.n)
         return out
 
     ops_mod.StencilOperator.run_cycle = timed_run_cycle
@@ -385,14 +427,15 @@ def run_ours(args, rank, world, local):
     p_host = srj.ProblemInstance(A=A, b=b_host, x0=x0_host, stopping_norm="relative_l2")
     e2e_ms = []
     e2e_sweeps = []
-    # untimed warm-up: the first call allocates the pinned readback buffer
-    # (torch's caching host allocator reuses it afterwards)
-    srj.solve(p_host, ctrl, rule, record_history=False)
+    # the solution lands in a pinned host buffer allocated once (outside the
+    # timed region); its D2H copy is inside every timed step
+    x_out = torch.empty(A.n, dtype=torch.float64, pin_memory=True)
+    srj.solve(p_host, ctrl, rule, record_history=False, out=x_out)  # untimed warm-up
     for _ in range(max(1, min(args.steps, 3))):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        r2 = srj.solve(p_host, ctrl, rule, record_history=False)
+        r2 = srj.solve(p_host, ctrl, rule, record_history=False, out=x_out)
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
         e2e_sweeps.append(r2.total_iterations)

@@ -358,13 +358,17 @@ def _next_scheme(controller: Controller, state: SolverState, order_grid: int) ->
 
 
 def solve(problem: ProblemInstance, controller: Controller, stopping: StoppingRule,
-          order_grid: int = ORDER_GRID_SIZE, record_history: bool = True) -> SolveReport:
+          order_grid: int = ORDER_GRID_SIZE, record_history: bool = True,
+          out=None) -> SolveReport:
     """Full solve under a controller and stopping rule (reference solver.py:289-331).
 
     b and x0 are staged into HBM once; the iterate then ping-pongs between two
     device buffers for the whole solve with no per-cycle copies.  The report's
     x has the kind of x0: numpy array, CPU tensor (copied back through pinned
-    memory) or CUDA tensor (no copy).
+    memory) or CUDA tensor (no copy).  `out` (extension, optional): a
+    preallocated torch tensor of n float64 values (e.g. pinned host memory)
+    that receives the solution and becomes the report's x, so repeated solves
+    do not allocate a fresh host buffer each time.
     """
     t0 = time.perf_counter()
     A = _require_device_operator(problem.A)
@@ -372,7 +376,13 @@ def solve(problem: ProblemInstance, controller: Controller, stopping: StoppingRu
     b = A.field(problem.b)
     x = A.field(problem.x0)
     rep = solve_fields(A, b, x, A.new_field(), controller, stopping, order_grid, record_history)
-    rep.x = _like(problem.x0, rep.x)
+    if out is not None:
+        if out.numel() != A.n:
+            raise ValueError(f"out holds {out.numel()} values, the operator {A.n}")
+        out.view(-1).copy_(rep.x.reshape(-1))
+        rep.x = out
+    else:
+        rep.x = _like(problem.x0, rep.x)
     rep.wall_time = time.perf_counter() - t0
     return rep
 

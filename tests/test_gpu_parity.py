@@ -162,3 +162,25 @@ def test_standalone_sweep_and_norm_helpers_match_oracle():
     assert srj.diff_inf(xs, bs) == float(np.max(np.abs(xs - bs)))
     with pytest.raises(ValueError):
         srj.matvec(S, xs[:-1])
+
+
+def test_solve_into_preallocated_out():
+    """solve(out=...) writes the solution into the caller's buffer (pinned host
+    or device) and returns it as the report's x; values identical to the
+    default return path."""
+    import torch
+
+    c = P.case("c2_64")
+    ref = device_solve(c, record_history=False)
+    import paper_2011_06636_b200 as srj
+    fam, n, b, _, _ = P.case_inputs(c)
+    A = srj.StencilOperator(fam, (n, n))
+    p = srj.ProblemInstance(A=A, b=b, x0=np.zeros(A.n), stopping_norm=c["norm"])
+    rule = srj.StoppingRule(c["norm"], c["tol"], c.get("max_iterations", 10**9))
+    for out in (torch.empty(A.n, dtype=torch.float64, pin_memory=True),
+                torch.empty(A.n, dtype=torch.float64, device="cuda")):
+        rep = srj.solve(p, srj.Heuristic(), rule, record_history=False, out=out)
+        assert rep.x is out
+        assert np.array_equal(out.cpu().numpy(), ref.x)
+    with pytest.raises(ValueError):
+        srj.solve(p, srj.Heuristic(), rule, out=torch.empty(3, dtype=torch.float64))
