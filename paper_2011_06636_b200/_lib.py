@@ -66,7 +66,8 @@ class OpInfo(ctypes.Structure):
                3: "srj::k_cycle3d (TMA plane ring)",
                4: "srj::k_ws2d_cycle (warp-streaming temporal blocking)",
                5: "srj::k_tb3d_cycle (TMA z-wavefront temporal blocking)",
-               6: "srj::k_tbvar_cycle (TMA var-coef temporal blocking)"}
+               6: "srj::k_tbvar_cycle (TMA var-coef temporal blocking)",
+               7: "srj::k_small_cycle_1d (single-CTA shared-memory cycle)"}
 
     def as_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
