@@ -462,11 +462,12 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("3D temporal-blocking setup failed: ") + cudaGetErrorString(e));
     }
-    // Default: 4 fused sweeps per pass where the 2D temporally blocked kernel
-    // exists, else one per pass.  3D keeps the HBM-bound plane ring by default:
-    // the z-wavefront TB kernel (sweeps_per_pass 2) measured slower on B200
-    // (DESIGN.md §4).
-    op->sweeps_per_pass = (op->tb.supported || op->ws.supported || op->tbv.supported) ? 4 : 1;
+    // Default: fused sweeps where a 2D temporally blocked kernel exists (6 per
+    // pass for constant coefficients -- the S=6 tile variant measured fastest
+    // on B200 -- 4 for variable coefficients), else one per pass.  3D keeps the
+    // HBM-bound plane ring by default: the z-wavefront TB kernel (sweeps_per_pass
+    // 2) measured slower on B200.
+    op->sweeps_per_pass = op->tb.supported ? 6 : (op->ws.supported || op->tbv.supported) ? 4 : 1;
     op->slot_capacity = std::max(op->p3.slots, kApplyBlocksPerSm * op->num_sms);
     for (int s = 0; s < kSlots; ++s) {
         if ((e = cudaMalloc(&op->slot_part[s], op->slot_capacity * sizeof(double))) != cudaSuccess) {
@@ -531,11 +532,12 @@ int srj_op_describe(const srj_op* op, srj_op_info* info) {
     info->cycle_threads = op->coop_threads;
     info->sweeps_per_pass = op->sweeps_per_pass;
     info->tb_supported = (op->tb.supported || op->tb3.supported || op->tbv.supported) ? 1 : 0;
+    const int tbk = tb_variant_for(op->tb, op->sweeps_per_pass);
     info->tb_blocks = op->tbv.supported ? op->tbv.blocks
-                      : op->tb3.supported ? op->tb3.blocks : op->tb.blocks[op->tb.small_variant];
+                      : op->tb3.supported ? op->tb3.blocks : op->tb.blocks[tbk];
     info->tb_occupancy = (op->tbv.supported || op->tb3.supported) ? 1 : op->tb.occupancy;
     info->tb_tiles = op->tbv.supported ? op->tbv.ntiles
-                     : op->tb3.supported ? op->tb3.ntiles : op->tb.ntiles[op->tb.small_variant];
+                     : op->tb3.supported ? op->tb3.ntiles : op->tb.ntiles[tbk];
     info->cycle_kernel = (op->sweeps_per_pass > 1 && op->tbv.supported)  ? SRJ_KERNEL_TBVAR
                          : (op->sweeps_per_pass > 1 && op->tb3.supported) ? SRJ_KERNEL_TB3D
                          : op->p3.supported                               ? SRJ_KERNEL_PLANE3D

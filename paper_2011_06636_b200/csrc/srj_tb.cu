@@ -81,10 +81,13 @@ struct Cfg;
 template <>
 struct Cfg<0> : CfgBase<4, 2, 6, 12> {};  // 64x72 region, 56x64 tile, 384 threads
 template <>
-struct Cfg<1> : CfgBase<4, 2, 9, 8> {};   // 64x72 region, 56x64 tile, 256 threads
-// Measured on B200 (2048^2 / 4096^2, us per sweep): K=0 9.4 / 33.5, K=1
-// 10.2 / 36.7; 16-warp 64x96 and 18-warp 64x72 shapes spill (10.9 / 38.4),
-// 64x128 spills heavily (15.7), 4 columns per lane (128x72) spills (15.0).
+struct Cfg<1> : CfgBase<6, 2, 6, 12> {};  // 64x72 region, 52x60 tile, 384 threads (S = 6)
+// The variant follows the requested sweeps per pass: s <= 4 -> K=0, s = 5, 6
+// -> K=1.  Measured on B200 (2048^2 / 4096^2, us per sweep): K=0 at s=4 9.4 /
+// 33.5, K=1 at s=6 9.2 / 30.7; an S=8 ring (48x56 tiles) 9.8 / 34.7 at s=8,
+// 8 warps x 9 rows at S=4 9.7 / 35.0; 16-warp 64x96 and 18-warp 64x72 shapes
+// spill (10.9 / 38.4), 64x128 spills heavily (15.7), 4 columns per lane
+// (128x72) spills (15.0).
 constexpr int kVariants = 2;
 
 }  // namespace tb2d
@@ -295,6 +298,8 @@ __device__ __forceinline__ void tile_dispatch(int h, TileRegs<K>& R, const doubl
         SRJ_TB_CASE(2)
         SRJ_TB_CASE(3)
         SRJ_TB_CASE(4)
+        SRJ_TB_CASE(5)
+        SRJ_TB_CASE(6)
         default: break;
     }
 #undef SRJ_TB_CASE
@@ -512,6 +517,11 @@ static void plan_tiles(TbPlan& plan, const Geom& g, int num_sms) {
     plan.blocks[K] = std::max(1, std::min(num_sms, plan.ntiles[K]));
 }
 
+int tb_variant_for(const TbPlan& plan, int s) {
+    if (plan.small_variant >= 0) return plan.small_variant;
+    return s > tb2d::Cfg<0>::S ? 1 : 0;
+}
+
 cudaError_t tb_plan_init(TbPlan& plan, const Geom& g, int num_sms) {
     plan = TbPlan();
     // TMA needs 16-byte row pitch: even nx.
@@ -520,13 +530,14 @@ cudaError_t tb_plan_init(TbPlan& plan, const Geom& g, int num_sms) {
     cudaError_t e;
     if ((e = setup_variant<0>(occ[0])) != cudaSuccess) return e;
     if ((e = setup_variant<1>(occ[1])) != cudaSuccess) return e;
-    // variant: SRJ_TB_VARIANT=k overrides the default (tuning only)
-    plan.small_variant = 0;
+    // variant: chosen per launch from the sweeps per pass; SRJ_TB_VARIANT=k
+    // forces one (tuning only)
+    plan.small_variant = -1;
     if (const char* v = getenv("SRJ_TB_VARIANT")) {
         const int k = atoi(v);
         if (k >= 0 && k < tb2d::kVariants) plan.small_variant = k;
     }
-    plan.occupancy = occ[plan.small_variant];
+    plan.occupancy = std::min(occ[0], occ[1]);
     if (plan.occupancy < 1) return cudaSuccess;
     plan_tiles<0>(plan, g, num_sms);
     plan_tiles<1>(plan, g, num_sms);
@@ -563,14 +574,15 @@ cudaError_t tb_launch_cycle(const TbPlan& plan, const Geom& g, double* x, double
     a.b = b;
     a.omegas = omegas;
     a.M = M;
-    a.s = std::max(1, std::min(s, 4));  // the variants fuse at most 4 sweeps
+    const int k = tb_variant_for(plan, s);
+    a.s = std::max(1, std::min(s, k == 1 ? tb2d::Cfg<1>::S : tb2d::Cfg<0>::S));
     a.tol = tol;
     a.baseline = baseline;
     a.partials = partials;
     a.hist = hist;
     a.out_i = out_i;
     a.out_d = out_d;
-    switch (plan.small_variant) {
+    switch (k) {
         case 1: return launch_variant<1>(plan, g, a, x, x_alt, b, st);
         default: return launch_variant<0>(plan, g, a, x, x_alt, b, st);
     }

@@ -16,12 +16,15 @@ struct TbPlan {
     int blocks[8] = {};   // cooperative grid (one CTA per SM)
     int tiles_x[8] = {};
     int ntiles[8] = {};
-    int small_variant = 1;          // variant launched (tb2d::Cfg<K>)
+    int small_variant = -1;         // forced variant (SRJ_TB_VARIANT), -1: by sweeps per pass
     int occupancy = 0;              // min resident CTAs per SM over the variants
 };
 
 // Decide whether the operator has a temporal-blocking kernel and size its grid.
 cudaError_t tb_plan_init(TbPlan& plan, const Geom& g, int num_sms);
+// Kernel variant (tb2d::Cfg<K>) serving s sweeps per pass: K=0 (S=4 ring)
+// for s <= 4, K=1 (S=6 ring) for s = 5, 6.
+int tb_variant_for(const TbPlan& plan, int s);
 
 // Launch one cycle of M sweeps, s per pass (1 <= s <= kTbMaxSub; the 2D
 // kernel fuses at most 4 and clamps larger requests).  Same
