@@ -462,12 +462,12 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("3D temporal-blocking setup failed: ") + cudaGetErrorString(e));
     }
-    // Default: fused sweeps where a 2D temporally blocked kernel exists (6 per
-    // pass for constant coefficients -- the S=6 tile variant measured fastest
-    // on B200 -- 4 for variable coefficients), else one per pass.  3D keeps the
+    // Default: 6 fused sweeps per pass where a 2D temporally blocked kernel
+    // exists (the S=6 rings measured fastest on B200 for constant and variable
+    // coefficients), else one per pass.  3D keeps the
     // HBM-bound plane ring by default: the z-wavefront TB kernel (sweeps_per_pass
     // 2) measured slower on B200.
-    op->sweeps_per_pass = op->tb.supported ? 6 : (op->ws.supported || op->tbv.supported) ? 4 : 1;
+    op->sweeps_per_pass = (op->tb.supported || op->tbv.supported) ? 6 : op->ws.supported ? 4 : 1;
     op->slot_capacity = std::max(op->p3.slots, kApplyBlocksPerSm * op->num_sms);
     for (int s = 0; s < kSlots; ++s) {
         if ((e = cudaMalloc(&op->slot_part[s], op->slot_capacity * sizeof(double))) != cudaSuccess) {

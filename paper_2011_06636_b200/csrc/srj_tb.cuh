@@ -53,7 +53,7 @@ cudaError_t tb3_launch_cycle(const Tb3Plan& plan, const Geom& g, double* x, doub
                              double baseline, double* partials, double* hist, int* out_i,
                              double* out_d, cudaStream_t st);
 
-// 2D variable-coefficient temporal blocking (srj_tbvar.cu), 4 sweeps per pass.
+// 2D variable-coefficient temporal blocking (srj_tbvar.cu), up to 6 sweeps per pass.
 struct TbvPlan {
     bool supported = false;
     int blocks = 0, tiles_x = 0, ntiles = 0;

@@ -1,9 +1,10 @@
 // Temporally blocked SRJ cycle for the 2D 5-point VARIABLE-coefficient stencil
-// (BASELINE config 4: -div(k grad u) = f with harmonic-mean faces): S = 4
-// consecutive sweeps, each with its own omega, per HBM round trip.
+// (BASELINE config 4: -div(k grad u) = f with harmonic-mean faces): S = 6
+// consecutive sweeps, each with its own omega, per HBM round trip.  Measured on
+// B200 at 4096^2 (us per sweep): S = 4 55.2, S = 6 49.4, S = 8 57.0.
 //
 // Same frame as the constant-coefficient kernel (srj_tb.cu): persistent
-// cooperative CTAs, 56x40 owned tiles in a 64x48 region (S-wide ring), TMA
+// cooperative CTAs, 52x36 owned tiles in a 64x48 region (S-wide ring), TMA
 // staging with the next tile's boxes loading while the current one computes,
 // a split barrier for the halo rows, one grid barrier per pass with the
 // fixed-order residual reduction, rollback of a pass that stops inside.
@@ -37,7 +38,7 @@ namespace srj {
 namespace tbv {
 
 struct Cfg {
-    static constexpr int S = 4, CW = 2, V = 6, NSEG = 8;
+    static constexpr int S = 6, CW = 2, V = 6, NSEG = 8;
     static constexpr int RX = 32 * CW, RY = NSEG * V;
     static constexpr int TX = RX - 2 * S, TY = RY - 2 * S;
     static constexpr int THREADS = 32 * NSEG;
@@ -221,6 +222,8 @@ __device__ __forceinline__ void tbv_dispatch(int h, TbvRegs& R, const double* om
         case 2: tbv_sweeps<2, MASKED>(R, omegas, warp, lane, inmask, accmask, acc, na); break;
         case 3: tbv_sweeps<3, MASKED>(R, omegas, warp, lane, inmask, accmask, acc, na); break;
         case 4: tbv_sweeps<4, MASKED>(R, omegas, warp, lane, inmask, accmask, acc, na); break;
+        case 5: tbv_sweeps<5, MASKED>(R, omegas, warp, lane, inmask, accmask, acc, na); break;
+        case 6: tbv_sweeps<6, MASKED>(R, omegas, warp, lane, inmask, accmask, acc, na); break;
         default: break;
     }
 }
