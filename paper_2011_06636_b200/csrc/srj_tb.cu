@@ -192,6 +192,12 @@ __device__ __forceinline__ void tile_sweeps(TileRegs<K>& R, const double* omegas
     using L = TbLayout<K>;
     constexpr int V = C::V, CW = C::CW, RX = C::RX;
     static_assert(V >= 3 && CW == 2, "row-pair groups of a 2-column lane");
+    // Ring and tile aligned to warps (rows) and lanes (columns): a thread owns
+    // all of its points or none, so unmasked tiles accumulate r^2
+    // unconditionally and select once per sub-sweep (S = 6 ring with 6 rows
+    // per warp: warps 0 and NSEG-1 own nothing, lanes 0-2 and 29-31 own nothing).
+    constexpr bool kAligned = C::S % V == 0 && C::TY % V == 0 && C::S % CW == 0 &&
+                              C::TX % CW == 0;
     const double coff = g.c_off, cdiag = g.c_diag, inv = g.inv_diag;
     const int col = lane * CW;
 #pragma unroll
@@ -254,7 +260,10 @@ __device__ __forceinline__ void tile_sweeps(TileRegs<K>& R, const double* omegas
                 const int v = k < 2 ? va : vb, j = k & 1;
                 const int bit = v * CW + j;
                 const double xn = relax(R.x[v][j], inv, rr[k], w);
-                fma_sq_if(sq[k], rr[k], (accmask >> bit) & 1u);
+                if constexpr (!MASKED && kAligned)
+                    sq[k] = fma(rr[k], rr[k], sq[k]);  // owned: decided per thread below
+                else
+                    fma_sq_if(sq[k], rr[k], (accmask >> bit) & 1u);
                 R.x[v][j] = (!MASKED || ((inmask >> bit) & 1u)) ? xn : 0.0;
             }
         };
@@ -268,7 +277,11 @@ __device__ __forceinline__ void tile_sweeps(TileRegs<K>& R, const double* omegas
         lds_cols<CW>(hs, L::bot(t) + warp * RX + col);        // bottom row of warp-1
         lds_cols<CW>(hn, L::top(t) + (warp + 2) * RX + col);  // top row of warp+1
         group(0, V - 1);
-        acc[t] = DADD(acc[t], DADD(DADD(sq[0], sq[1]), DADD(sq[2], sq[3])));
+        if constexpr (!MASKED && kAligned)
+            acc[t] = accmask != 0u ? DADD(acc[t], DADD(DADD(sq[0], sq[1]), DADD(sq[2], sq[3])))
+                                   : acc[t];
+        else
+            acc[t] = DADD(acc[t], DADD(DADD(sq[0], sq[1]), DADD(sq[2], sq[3])));
 #pragma unroll
         for (int v = 0; v < V; ++v)
 #pragma unroll

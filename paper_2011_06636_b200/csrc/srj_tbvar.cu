@@ -137,6 +137,10 @@ __device__ __forceinline__ void tbv_sweeps(TbvRegs& R, const double* omegas, int
     using C = tbv::Cfg;
     using L = TbvLayout;
     constexpr int V = C::V, CW = C::CW, RX = C::RX;
+    // ring and tile aligned to warps and lanes: a thread owns all of its
+    // points or none (see srj_tb.cu), so unmasked tiles select once per sub-sweep
+    constexpr bool kAligned = C::S % V == 0 && C::TY % V == 0 && C::S % CW == 0 &&
+                              C::TX % CW == 0;
     const int col = lane * CW;
 #pragma unroll
     for (int t = 0; t < H; ++t) {
@@ -168,7 +172,10 @@ __device__ __forceinline__ void tbv_sweeps(TbvRegs& R, const double* omegas, int
                 const double rr = DSUB(R.b[v][j], y);
                 const double xnew = relax(R.x[v][j], R.inv[v][j], rr, w);
                 const int bit = v * CW + j;
-                fma_sq_ifv(sq[j], rr, (accmask >> bit) & 1u);
+                if constexpr (!MASKED && kAligned)
+                    sq[j] = fma(rr, rr, sq[j]);  // owned: decided per thread below
+                else
+                    fma_sq_ifv(sq[j], rr, (accmask >> bit) & 1u);
                 xo[j] = (!MASKED || ((inmask >> bit) & 1u)) ? xnew : 0.0;
             }
 #pragma unroll
@@ -203,7 +210,10 @@ __device__ __forceinline__ void tbv_sweeps(TbvRegs& R, const double* omegas, int
         ld2(hn, L::top(t) + (warp + 2) * RX + col);  // top row of warp+1
         row(0, hs, old_r1);
         row(V - 1, old_rl, hn);
-        acc[t] = DADD(acc[t], DADD(sq[0], sq[1]));
+        if constexpr (!MASKED && kAligned)
+            acc[t] = accmask != 0u ? DADD(acc[t], DADD(sq[0], sq[1])) : acc[t];
+        else
+            acc[t] = DADD(acc[t], DADD(sq[0], sq[1]));
         if (t + 1 < H) {
             st2(L::top(t + 1) + (warp + 1) * RX + col, R.x[0]);
             st2(L::bot(t + 1) + (warp + 1) * RX + col, R.x[V - 1]);
