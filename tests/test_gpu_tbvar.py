@@ -42,8 +42,11 @@ def _oracle_sweeps(op, x, b, omegas, baseline):
     return xs, res
 
 
-@pytest.mark.parametrize("dims", [(130, 90), (64, 41), (58, 200), (2, 2)])
-def test_tbvar_cycle_bitwise_vs_oracle(dims):
+@pytest.mark.parametrize("dims,kernel", [((130, 90), 6), ((64, 41), 6), ((58, 200), 6),
+                                         ((2, 2), 6), ((400, 1), 6), ((33, 17), 0)])
+def test_tbvar_cycle_bitwise_vs_oracle(dims, kernel):
+    """kernel 6: k_tbvar_cycle; odd nx (no 16-byte TMA row pitch for any tile
+    kernel) falls back to the generic row walker k_cycle (0)."""
     import torch
 
     import paper_2011_06636_b200 as srj
@@ -54,7 +57,7 @@ def test_tbvar_cycle_bitwise_vs_oracle(dims):
     fx = rng.uniform(0.5, 30.0, (ny, nx + 1))
     fy = rng.uniform(0.5, 30.0, (ny + 1, nx))
     A = srj.StencilOperator("2d5var", dims, face_x=fx, face_y=fy, device=dev)
-    assert A.describe()["cycle_kernel"] == 6  # k_tbvar_cycle
+    assert A.describe()["cycle_kernel"] == kernel
     op = O.StencilCPU("2d5var", nx, ny, 1, 0.0, fx, fy)
     b = rng.uniform(-1, 1, A.n)
     x0 = rng.uniform(-1, 1, A.n)
