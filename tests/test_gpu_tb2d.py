@@ -1,0 +1,68 @@
+"""Constant-coefficient 2D temporal blocking (srj_tb.cu) vs the oracle, cycle by cycle.
+
+Both tile variants (S = 4 ring for <= 4 sweeps per pass, S = 6 ring for 5-6)
+on multi-tile, non-square, single-row and odd-nx grids, with every stop
+position inside a pass (rollback) exercised; the golden solves in
+test_gpu_parity.py cover the reference traces.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_sweeps(op, x, b, omegas, baseline):
+    xs, res = [x], []
+    for w in omegas:
+        r, s = op.residual(xs[-1], b)
+        res.append(math.sqrt(s) / baseline)
+        xs.append(op.update(xs[-1], r, w))
+    _, s = op.residual(xs[-1], b)
+    res.append(math.sqrt(s) / baseline)
+    return xs, res
+
+
+@pytest.mark.parametrize("spp", [4, 6])
+@pytest.mark.parametrize("dims,kernel", [((130, 90), 1), ((64, 41), 1), ((2, 300), 1),
+                                         ((400, 1), 1), ((33, 17), 0)])
+def test_tb2d_cycle_bitwise_vs_oracle(dims, kernel, spp):
+    import torch
+
+    import paper_2011_06636_b200 as srj
+    from oracle import srj_oracle as O
+    nx, ny = dims
+    dev = torch.device("cuda", 0)
+    A = srj.StencilOperator("2d5", dims, dx2=5.0, device=dev)
+    A.set_sweeps_per_pass(spp)
+    assert A.describe()["cycle_kernel"] == kernel
+    op = O.StencilCPU("2d5", nx, ny, 1, 5.0)
+    rng = np.random.default_rng(nx * 1000 + ny + spp)
+    b = rng.uniform(-1, 1, A.n)
+    x0 = rng.uniform(-1, 1, A.n)
+    omegas = rng.uniform(0.4, 2.6, 13)
+    baseline = 3.0
+    xs, res = _oracle_sweeps(op, x0, b, omegas, baseline)
+    om = torch.tensor(omegas, dtype=torch.float64, device=dev)
+    bf = A.field(b)
+    for stop in [None] + list(range(1, 13)):
+        if stop is None:
+            tol = 0.0
+        else:
+            tol = res[stop] * (1.0 + 1e-9)  # margin above the norm-order difference
+            if any(r <= tol * (1.0 + 1e-9) for r in res[:stop]):
+                continue
+        x = A.field(x0)
+        x_alt = A.new_field()
+        hist = np.zeros(len(omegas))
+        out = A.run_cycle(x, x_alt, bf, om, len(omegas), tol, baseline, res[0], 10**9, hist)
+        k = len(omegas) if stop is None else stop
+        assert out.executed == k, (stop, out.executed)
+        got = (x_alt if out.result_in_alt else x).interior.cpu().numpy()
+        assert np.array_equal(got, xs[k]), (stop, np.max(np.abs(got - xs[k])))
+        np.testing.assert_allclose(hist[:k], res[1:k + 1], rtol=1e-12)
+        np.testing.assert_allclose(out.res_after, res[k], rtol=1e-12)
