@@ -40,6 +40,7 @@
 
 #include "srj_stencil.cuh"
 #include "srj_tb.cuh"
+#include "srj_tbdriver.cuh"
 #include "srj_tma.cuh"
 #include "srj_walk.cuh"
 
@@ -76,20 +77,8 @@ using C2 = Cfg<2, 16, 2>;  // 64x32 region, 60x28 tile, 512 threads
 
 }  // namespace tb3d
 
-struct Tb3Args {
-    Geom g;
-    double* buf0;
-    double* buf1;
-    const double* b;
-    const double* omegas;
-    int M, s;
-    double tol, baseline;
-    double* partials;  // [2][kTbMaxSub][gridDim.x]
-    double* hist;
-    int* out_i;
-    double* out_d;
-    int tiles_x, ntiles;
-};
+using Tb3Args = TbArgs;
+
 
 extern __shared__ __align__(128) double tb3_smem[];
 
@@ -334,9 +323,6 @@ __global__ void __launch_bounds__(C::THREADS, 1) __maxnreg__(C::MAXREG)
                  const __grid_constant__ CUtensorMap tm_b, Tb3Args a) {
     using L = Tb3Layout<C>;
     constexpr int S = C::S;
-    __shared__ double sh[32 * S];
-    __shared__ double red[S];
-    __shared__ double sh1[32];
     // zero edge rows (the rows beyond the first and last warp are never written)
     for (int i = threadIdx.x; i < 2 * S * C::HB; i += blockDim.x) L::top(0, 0)[i] = 0.0;
     if (threadIdx.x == 0) {
@@ -357,72 +343,14 @@ __global__ void __launch_bounds__(C::THREADS, 1) __maxnreg__(C::MAXREG)
                     ownmask |= 1u << (v * C::CW + j);
     }
     uint32_t ph = 0;
-    const int nb = gridDim.x;
-    double* const buf[2] = {a.buf0, a.buf1};
     const CUtensorMap* const tmx[2] = {&tm_x0, &tm_x1};
-    const int npasses = (a.M + a.s - 1) / a.s;
-    int executed = a.M, status = kStatusRan, result = npasses & 1;
-    double S2 = 0.0, res = 0.0;
-    bool stopped = false;
-    for (int p = 0; p < npasses && !stopped; ++p) {
-        const int k0 = p * a.s;
-        const int h = min(a.s, a.M - k0);
-        double acc[S];
-#pragma unroll
-        for (int t = 0; t < S; ++t) acc[t] = 0.0;
-        tb3_pass<C>(a, tmx[p & 1], &tm_b, buf[(p + 1) & 1], k0, h, acc, true, ownmask, ph);
-        double* part = a.partials + (size_t)(p & 1) * kTbMaxSub * nb;
-        block_sums<S>(acc, h, sh, red);
-        if (threadIdx.x < h) part[threadIdx.x * nb + blockIdx.x] = red[threadIdx.x];
-        grid_barrier();
-        reduce_partials_multi(part, nb, h, red);
-        int stop_t = -1;
-        for (int t = 0; t < h; ++t) {
-            const int k = k0 + t;
-            if (k == 0) continue;  // res(x_0) is known to the host
-            S2 = red[t];
-            res = sqrt(S2) / a.baseline;
-            if (blockIdx.x == 0 && threadIdx.x == 0) a.hist[k] = res;
-            if (!isfinite(res)) { status = kStatusDiverged; stop_t = t; break; }
-            if (res <= a.tol) { status = kStatusConverged; stop_t = t; break; }
-        }
-        __syncthreads();  // red[] is reused below
-        if (stop_t >= 0) {
-            stopped = true;
-            executed = k0 + stop_t;
-            if (stop_t == 0) {
-                result = p & 1;
-            } else {
-                // rollback: x_{k0+stop_t} from the intact pass input
-                tb3_pass<C>(a, tmx[p & 1], &tm_b, buf[(p + 1) & 1], k0, stop_t, acc, false,
-                            ownmask, ph);
-                grid_barrier();
-                result = (p + 1) & 1;
-            }
-        }
-    }
-    if (!stopped) {
-        // residual of the cycle's final iterate (solver.py:233-234,248-249)
-        const int u0 = (int)((long long)a.g.units * blockIdx.x / nb);
-        const int u1 = (int)((long long)a.g.units * (blockIdx.x + 1) / nb);
-        double acc = walk_units<F3D, kResid>(a.g, buf[result], nullptr, a.b, 0.0, u0, u1);
-        double* part = a.partials + (size_t)(npasses & 1) * kTbMaxSub * nb;
-        acc = block_allsum(acc, sh1);
-        if (threadIdx.x == 0) part[blockIdx.x] = acc;
-        grid_barrier();
-        S2 = reduce_partials(part, nb, sh1);
-        res = sqrt(S2) / a.baseline;
-        if (blockIdx.x == 0 && threadIdx.x == 0) a.hist[a.M] = res;
-        if (!isfinite(res)) status = kStatusDiverged;
-        else if (res <= a.tol) status = kStatusConverged;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        a.out_i[0] = executed;
-        a.out_i[1] = status;
-        a.out_i[2] = result;
-        a.out_d[0] = S2;
-        a.out_d[1] = res;
-    }
+    // tiles load their own planes (tile prologue): no speculative first-tile load
+    tb_run_cycle<S, F3D>(
+        a,
+        [&](int in, double* xout, int k0, int h, double (&acc)[S], bool accumulate, bool) {
+            tb3_pass<C>(a, tmx[in], &tm_b, xout, k0, h, acc, accumulate, ownmask, ph);
+        },
+        [](int, int) {}, []() {});
 }
 
 // ----------------------------------------------------------------------------
