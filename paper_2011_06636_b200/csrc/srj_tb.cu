@@ -413,12 +413,12 @@ __global__ void __launch_bounds__(tb2d::Cfg<K>::THREADS, 1) __maxnreg__(tb2d::Cf
     uint32_t phase = 0, na = 0;
     const CUtensorMap* const tmx[2] = {&tm_x0, &tm_x1};
     tb_run_cycle<S, F2D>(
-        a,
+        a, (int)blockIdx.x < a.ntiles,
         [&](int in, double* xout, int k0, int h, double (&acc)[S], bool accumulate, bool first) {
             tb2d_pass<K>(a, tmx[in], &tm_b, xout, k0, h, acc, accumulate, ownmask, phase, first,
                          na);
         },
-        [&](int in, int q) { tb2d_issue<K>(a, tmx[in], &tm_b, q); },
+        [&](int in) { tb2d_issue<K>(a, tmx[in], &tm_b, blockIdx.x); },
         [&]() {
             mbar_wait(L::bar(), phase);
             phase ^= 1u;

@@ -346,11 +346,11 @@ __global__ void __launch_bounds__(C::THREADS, 1) __maxnreg__(C::MAXREG)
     const CUtensorMap* const tmx[2] = {&tm_x0, &tm_x1};
     // tiles load their own planes (tile prologue): no speculative first-tile load
     tb_run_cycle<S, F3D>(
-        a,
+        a, (int)blockIdx.x < a.ntiles,
         [&](int in, double* xout, int k0, int h, double (&acc)[S], bool accumulate, bool) {
             tb3_pass<C>(a, tmx[in], &tm_b, xout, k0, h, acc, accumulate, ownmask, ph);
         },
-        [](int, int) {}, []() {});
+        [](int) {}, []() {});
 }
 
 // ----------------------------------------------------------------------------

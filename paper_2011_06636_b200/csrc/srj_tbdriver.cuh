@@ -37,11 +37,12 @@ struct TbArgs {
 // pass(in, xout, k0, h, acc, accumulate, first_issued): one pass of h
 //   sub-sweeps over this CTA's tiles, reading buffer `in` (0: buf0, 1: buf1)
 //   and writing xout; acc[t] += owned r^2 of sub-sweep t when accumulating.
-// issue(in, q): (thread 0) start the TMA of tile q of buffer `in`.
+// issue(in): (thread 0) start the TMA of this CTA's first tile of buffer `in`.
 // drain(): every thread waits for the outstanding TMA.
+// has_tiles: this CTA owns at least one tile.
 template <int S, int FAM, class Pass, class Issue, class Drain>
-__device__ __forceinline__ void tb_run_cycle(const TbArgs& a, Pass&& pass, Issue&& issue,
-                                             Drain&& drain) {
+__device__ __forceinline__ void tb_run_cycle(const TbArgs& a, bool has_tiles, Pass&& pass,
+                                             Issue&& issue, Drain&& drain) {
     __shared__ double sh[32 * S];
     __shared__ double red[S];
     __shared__ double sh1[32];
@@ -64,8 +65,8 @@ __device__ __forceinline__ void tb_run_cycle(const TbArgs& a, Pass&& pass, Issue
         if (threadIdx.x < h) part[threadIdx.x * nb + blockIdx.x] = red[threadIdx.x];
         grid_barrier();
         // Speculatively start the next pass's first tile while the stop test runs.
-        if (p + 1 < npasses && (int)blockIdx.x < a.ntiles) {
-            if (threadIdx.x == 0) issue((p + 1) & 1, blockIdx.x);
+        if (p + 1 < npasses && has_tiles) {
+            if (threadIdx.x == 0) issue((p + 1) & 1);
             issued = true;
         }
         reduce_partials_multi(part, nb, h, red);

@@ -331,11 +331,11 @@ __global__ void __launch_bounds__(tbv::Cfg::THREADS, 1)
     uint32_t phase = 0, na = 0;
     const CUtensorMap* const tmx[2] = {&m.x0, &m.x1};
     tb_run_cycle<S, F2DV>(
-        a,
+        a, (int)blockIdx.x < a.ntiles,
         [&](int in, double* xout, int k0, int h, double (&acc)[S], bool accumulate, bool first) {
             tbv_pass(a, tmx[in], m, xout, k0, h, acc, accumulate, ownmask, phase, first, na);
         },
-        [&](int in, int q) { tbv_issue(a, tmx[in], m, q); },
+        [&](int in) { tbv_issue(a, tmx[in], m, blockIdx.x); },
         [&]() {
             mbar_wait(L::bar(), phase);
             phase ^= 1u;
