@@ -148,8 +148,9 @@ __global__ void __launch_bounds__(kSmall1dThreads) k_small_cycle_1d(CycleArgs a)
     extern __shared__ double sm[];
     __shared__ double red[2][32];
     const int n = a.g.nx;
-    double* const buf[2] = {sm + 1, sm + n + 3};  // interior starts; ghosts at [-1] and [n]
-    double* const bs = sm + 2 * (n + 2);
+    // buffer k (ping-pong) starts at offset base(k); ghosts at base-1 and base+n.
+    // Offsets, not pointers, keep every access an LDS/STS.
+    const int base0 = 1, base1 = n + 3, bso = 2 * (n + 2);
     const double c = a.g.c_off, d = a.g.c_diag, inv = a.g.inv_diag;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(kSmall1dThreads) k_small_cycle_1d(CycleArgs a)
         sm[i] = (i >= 1 && i <= n) ? a.xa[i - 1] : 0.0;
         sm[n + 2 + i] = 0.0;
     }
-    for (int i = threadIdx.x; i < n; i += blockDim.x) bs[i] = a.b[i];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sm[bso + i] = a.b[i];
     // S above `hi2` proves sqrt(S)/baseline > tol (1e-12 relative margin for the
     // two roundings); only S below it (or non-finite / huge) takes the exact path
     const double tb = a.tol * a.baseline;
@@ -167,16 +168,17 @@ __global__ void __launch_bounds__(kSmall1dThreads) k_small_cycle_1d(CycleArgs a)
     double S = 0.0;
     for (int k = 0; k <= a.M; ++k) {
         const bool tail = (k == a.M);
-        const double* xin = buf[k & 1];
-        double* xo = buf[(k + 1) & 1];
+        const int bi = (k & 1) ? base1 : base0;
+        const int bo = (k & 1) ? base0 : base1;
         const double w = tail ? 0.0 : __ldg(a.omegas + k);
         double acc = 0.0;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            double y = DADD(0.0, DMUL(c, xin[i - 1]));
-            y = DADD(y, DMUL(d, xin[i]));
-            y = DADD(y, DMUL(c, xin[i + 1]));
-            const double r = DSUB(bs[i], y);
-            if (!tail) xo[i] = relax(xin[i], inv, r, w);
+            const double xl = sm[bi + i - 1], xc = sm[bi + i], xr = sm[bi + i + 1];
+            double y = DADD(0.0, DMUL(c, xl));
+            y = DADD(y, DMUL(d, xc));
+            y = DADD(y, DMUL(c, xr));
+            const double r = DSUB(sm[bso + i], y);
+            if (!tail) sm[bo + i] = relax(xc, inv, r, w);
             acc = fma(r, r, acc);
         }
         acc = warp_allsum(acc);
@@ -193,12 +195,12 @@ __global__ void __launch_bounds__(kSmall1dThreads) k_small_cycle_1d(CycleArgs a)
             }
         }
     }
-    // x_executed lives in buf[executed & 1]; it goes to x (even) or x_alt
+    // x_executed lives in buffer executed & 1; it goes to x (even) or x_alt
     // (odd).  executed == 0 leaves x untouched (it is the input).
     if (executed > 0) {
-        const double* src = buf[executed & 1];
+        const int src = (executed & 1) ? base1 : base0;
         double* dst = (executed & 1) ? a.xb : const_cast<double*>(a.xa);
-        for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+        for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = sm[src + i];
     }
     __syncthreads();  // thread 0's hist stores are visible to the CTA
     for (int k = 1 + threadIdx.x; k <= last; k += blockDim.x) a.hist[k] = sqrt(a.hist[k]) / a.baseline;
