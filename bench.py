@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--planes-per-gpu", type=int, default=128, help="c5: z planes per GPU")
     ap.add_argument("--cycles", type=int, default=50, help="c5: heuristic cycles per step")
+    ap.add_argument("--slabs", action="store_true",
+                    help="c3/c4: use the slab solver even on one GPU (it is used for N > 1)")
     return ap.parse_args()
 
 
@@ -216,9 +218,13 @@ def run_reference(args, rank, world):
 
 
 def run_slabs(args, rank, world, local):
-    """Config 5 family: 3D Poisson z-slabs of nx x ny x planes_per_gpu on each of
-    N GPUs (N = 8: the 1024^3 grid of BASELINE config 5; N = 1: the 134M-point
-    per-GPU load of config 3), a fixed 50 heuristic cycles in throughput mode.
+    """Slab-decomposed solves, one process per GPU.
+
+    c5: 3D Poisson z-slabs of nx x ny x planes_per_gpu on each of N GPUs (N = 8:
+    the 1024^3 grid of BASELINE config 5; N = 1: the 134M-point per-GPU load of
+    config 3), a fixed 50 heuristic cycles in throughput mode (weak scaling).
+    c3 / c4 at N > 1: the config's fixed grid split into N z-slabs (3D) or row
+    slabs (2D variable coefficient), solved to the tolerance (strong scaling).
     Halo planes go over NCCL (torch.distributed P2P) overlapped with the
     interior planes' sweep; one all-gather of per-sweep partials per cycle."""
     import numpy as np
@@ -228,22 +234,36 @@ def run_slabs(args, rank, world, local):
     import paper_2011_06636_b200 as srj
     from paper_2011_06636_b200.distributed import (LocalExchanger, SlabSolver, TorchExchanger,
                                                    local_slabs)
+    from paper_2011_06636_b200.problems import CONFIGS, gaussian_field, harmonic_faces
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    nx = args.size or 1024
-    shape = (nx, nx, args.planes_per_gpu * world)
-    slabs = local_slabs("3d7", shape, world, [rank], dev)
+    throughput = args.config == "c5"
+    face_x = face_y = None
+    if throughput:
+        family = "3d7"
+        nx = args.size or 1024
+        shape = (nx, nx, args.planes_per_gpu * world)
+        rule = srj.StoppingRule("relative_l2", 1e-300, 10**9)
+        max_cycles = args.cycles
+    else:
+        family, extent, _ = CONFIGS[args.config]
+        n = args.size or extent
+        shape = (n, n, n) if family == "3d7" else (n, n)
+        if family == "2d5var":
+            face_x, face_y = harmonic_faces(np.exp(gaussian_field(n, args.seed)), (n + 1.0) ** 2)
+        rule = srj.StoppingRule("relative_l2", args.tol, 10**9)
+        max_cycles = None
+    slabs = local_slabs(family, shape, world, [rank], dev, face_x=face_x, face_y=face_y)
     ex = TorchExchanger() if world > 1 else LocalExchanger(1)
     solver = SlabSolver(slabs, ex)
-    rule = srj.StoppingRule("relative_l2", 1e-300, 10**9)
     ctrl = srj.Heuristic()
     stream = torch.cuda.current_stream(dev)
 
     def one():
         solver.load(seed=args.seed)
-        return solver.solve(ctrl, rule, record_history=False, max_cycles=args.cycles)
+        return solver.solve(ctrl, rule, record_history=False, max_cycles=max_cycles)
 
     for _ in range(args.warmup):
         one()
@@ -283,7 +303,7 @@ def run_slabs(args, rank, world, local):
         s0.x.buf.zero_()
         s0.x_alt.buf.zero_()
         s0.x.copy_(x0_host)
-        r = solver.solve(ctrl, rule, record_history=False, max_cycles=args.cycles)
+        r = solver.solve(ctrl, rule, record_history=False, max_cycles=max_cycles)
         x_out.copy_(r.x[0])
         return r
 
@@ -304,24 +324,28 @@ def run_slabs(args, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
     e2e_val = n_global * sum(e2e_sweeps) / (e2e_total * 1e-3) / 1e9
-    per_gpu_bytes = 24.0 * slabs[0].A.n * sum(sweeps)
+    per_gpu_bytes = float(BYTES_PER_UPDATE[family]) * slabs[0].A.n * sum(sweeps)
     peak, peak_kind = measured_peak()
     achieved = per_gpu_bytes / (total_ms * 1e-3) / 1e9
     line = {
-        "metric": METRIC["c5"],
+        "metric": METRIC["c5"] if throughput else METRIC["default"],
         "value": value, "unit": "GLUP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "weak" if throughput else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (f = 2u-1 from SplitMix64(seed), generated per slab on device)",
-        "config": {"workload": f"3D Poisson 7-pt {shape[0]}x{shape[1]}x{shape[2]} z-slabs "
-                               f"({args.planes_per_gpu} planes/GPU), {args.cycles} cycles",
-                   "sweeps_per_step": sweeps[-1], "cycles": len(rep.cycles),
+        "config": {"workload": (f"3D Poisson 7-pt {shape[0]}x{shape[1]}x{shape[2]} z-slabs "
+                                f"({args.planes_per_gpu} planes/GPU), {args.cycles} cycles")
+                               if throughput else CONFIG_DESC[args.config],
+                   "grid": list(shape), "sweeps_per_step": sweeps[-1], "cycles": len(rep.cycles),
                    "levels": [c.level for c in rep.cycles],
                    "executed": [c.executed for c in rep.cycles],
-                   "parallelism": f"z-slabs x{world}, NCCL halo P2P overlapped"},
+                   "time_to_tolerance_ms": None if throughput else total_ms / args.steps,
+                   "parallelism": f"{'z' if family == '3d7' else 'row'}-slabs x{world}, "
+                                  "NCCL halo P2P overlapped"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                     "kernel": "srj::k_sweep3d (slab sweep, whole step incl. exchange)"},
+                     "kernel": ("srj::k_sweep3d" if family == "3d7" else "srj::k_sweep2d")
+                               + " (slab sweep, whole step incl. exchange)"},
         "e2e": {"value": e2e_val, "unit": "GLUP/s", "h2d_bytes_per_step": 16 * s0.A.n * world,
                 "d2h_bytes_per_step": 8 * s0.A.n * world,
                 "ms_per_step": e2e_total / len(e2e_ms)},
@@ -494,7 +518,8 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if args.config == "c5":
+    # c5 always, and c3 / c4 on several GPUs (BASELINE: slab-sharded configs)
+    if args.config == "c5" or (args.config in ("c3", "c4") and (world > 1 or args.slabs)):
         run_slabs(args, rank, world, local)
         return
     run_ours(args, rank, world, local)
