@@ -257,6 +257,7 @@ cudaError_t plan3d_init(Plan3D& plan, const Geom& g, int num_sms) {
     plan.tiles_x = (g.nx + k3::TX - 1) / k3::TX;
     plan.tiles_y = (g.ny + k3::TY - 1) / k3::TY;
     plan.zc = choose_zc(plan, g.nz);
+    if (const char* v = getenv("SRJ_ZC")) plan.zc = std::max(1, std::min(atoi(v), g.nz));  // tuning
     plan.nzc = (g.nz + plan.zc - 1) / plan.zc;
     plan.items = plan.tiles_x * plan.tiles_y * plan.nzc;
     plan.blocks = std::max(1, std::min(plan.slots, plan.items));
