@@ -200,6 +200,17 @@ int64_t srj_op_planes(const srj_op* op);
 int srj_sweep_planes(srj_op* op, const double* x, double* x_out, const double* b,
                      double omega, int64_t z_begin, int64_t z_end, double* partial_dev,
                      int32_t slot, void* stream);
+/* Temporally blocked slab pass (2D constant or variable coefficient, even nx):
+ * h <= 6 consecutive sweeps with omegas_dev[0..h-1] over the operator's grid,
+ * storing only the owned rows [row_lo, row_hi) of x_alt (the rows outside are
+ * the deep ghost rows of a slab: updated as ring points, never stored).
+ * sums_dev[t] (device) = owned sum of (b - A x_t)^2 for t < h, reduced in a
+ * fixed order.  No stop test and no residual tail: the caller (the slab
+ * engine) decides per cycle.  Asynchronous.  Replaces, per slab, h iterations
+ * of solver.py:216-243 between two deep halo exchanges. */
+int srj_tb_pass(srj_op* op, double* x, double* x_alt, const double* b,
+                const double* omegas_dev, int32_t h, int64_t row_lo, int64_t row_hi,
+                double* sums_dev, void* stream);
 
 /* Batched small 1D Poisson cycles (data collection, datacollect.py:79-117:
  * the candidate cycles of many independent trials in one launch).  Job j

@@ -27,7 +27,7 @@ EXPORTED_SYMBOLS = (
     "srj_residual_sq",
     "srj_run_cycle", "srj_sweep", "srj_matvec", "srj_fill_uniform_rhs",
     "srj_op_planes", "srj_sweep_planes", "srj_run_cycle_diffinf", "srj_batch_cycles_1d",
-    "srj_op_set_temporal_kernel",
+    "srj_op_set_temporal_kernel", "srj_tb_pass",
 )
 TB_TILE, TB_WARP_STREAM = 0, 1
 
@@ -105,6 +105,8 @@ def _declare(L):
                                         POINTER(CycleOut), c_void_p]
     L.srj_sweep_planes.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int64,
                                    c_int64, c_void_p, c_int32, c_void_p]
+    L.srj_tb_pass.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
+                              c_int64, c_int64, c_void_p, c_void_p]
     for name in EXPORTED_SYMBOLS:
         if name not in ("srj_abi_version", "srj_last_error"):
             getattr(L, name).restype = c_int32

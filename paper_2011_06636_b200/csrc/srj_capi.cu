@@ -35,6 +35,7 @@ namespace cg = cooperative_groups;
 namespace srj {
 
 constexpr int kMaxSchemeLength = 10000;  // reference schemes.py:24
+constexpr int kTbPassMax = 6;             // sweeps one srj_tb_pass fuses (S = 6 rings)
 constexpr int kThreads = 256;       // standalone sweep / matvec kernels
 constexpr int kCoopThreads = 512;   // persistent cycle kernel: 2 CTAs per SM
 constexpr int kSmallThreads = 1024;
@@ -633,7 +634,7 @@ int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
     if (op->sweeps_per_pass > 1 && op->tbv.supported) {
         CUDA_TRY(tbv_launch_cycle(op->tbv, op->g, x, x_alt, b, omegas_dev, Meff,
                                   op->sweeps_per_pass, tol, baseline, op->partials, op->hist,
-                                  op->out_i, op->out_d, st));
+                                  op->out_i, op->out_d, st, 0, op->g.ny, nullptr));
         out->launches = 1;
     } else if (op->sweeps_per_pass > 1 && op->tb3.supported) {
         CUDA_TRY(tb3_launch_cycle(op->tb3, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,
@@ -651,7 +652,7 @@ int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
     } else if (op->sweeps_per_pass > 1 && op->tb.supported) {
         CUDA_TRY(tb_launch_cycle(op->tb, op->g, x, x_alt, b, omegas_dev, Meff,
                                  op->sweeps_per_pass, tol, baseline, op->partials, op->hist,
-                                 op->out_i, op->out_d, st));
+                                 op->out_i, op->out_d, st, 0, op->g.ny, nullptr));
         out->launches = 1;
     } else if (op->p2.supported) {
         CUDA_TRY(launch2d_cycle(op->p2, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,
@@ -713,6 +714,29 @@ int srj_run_cycle_diffinf(srj_op* op, double* x, double* x_alt, const double* b,
     out->res_after = op->h_out_d[1];
     if (history_host && out->executed > 0)
         std::memcpy(history_host, op->h_hist + 1, out->executed * sizeof(double));
+    return SRJ_OK;
+}
+
+int srj_tb_pass(srj_op* op, double* x, double* x_alt, const double* b,
+                const double* omegas_dev, int32_t h, int64_t row_lo, int64_t row_hi,
+                double* sums_dev, void* stream) {
+    if (!op || !x || !x_alt || !b || !omegas_dev || !sums_dev)
+        return fail(SRJ_BAD_ARGUMENT, "null argument");
+    if (!(op->tb.supported || op->tbv.supported))
+        return fail(SRJ_BAD_ARGUMENT, "no temporally blocked kernel for this operator");
+    if (h < 1 || h > kTbPassMax) return fail(SRJ_BAD_ARGUMENT, "sweeps per pass out of range");
+    if (row_lo < 0 || row_lo >= row_hi || row_hi > op->g.ny)
+        return fail(SRJ_BAD_ARGUMENT, "owned rows out of range");
+    DeviceGuard guard(op->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (op->tbv.supported)
+        CUDA_TRY(tbv_launch_cycle(op->tbv, op->g, x, x_alt, b, omegas_dev, h, h, -1.0, 1.0,
+                                  op->partials, op->hist, op->out_i, op->out_d, st, (int)row_lo,
+                                  (int)row_hi, sums_dev));
+    else
+        CUDA_TRY(tb_launch_cycle(op->tb, op->g, x, x_alt, b, omegas_dev, h, h, -1.0, 1.0,
+                                 op->partials, op->hist, op->out_i, op->out_d, st, (int)row_lo,
+                                 (int)row_hi, sums_dev));
     return SRJ_OK;
 }
 

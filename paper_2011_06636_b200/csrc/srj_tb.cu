@@ -135,13 +135,13 @@ __device__ __forceinline__ void sts_cols(double* p, const double (&d)[CW]) {
     for (int j = 0; j < CW; j += 2) *reinterpret_cast<double2*>(p + j) = make_double2(d[j], d[j + 1]);
 }
 
-template <int K>
+template <int K, bool SLAB>
 __device__ __forceinline__ void tb2d_issue(const TbArgs& a, const CUtensorMap* tm_in,
                                            const CUtensorMap* tm_b, int q) {
     using C = tb2d::Cfg<K>;
     using L = TbLayout<K>;
     constexpr int S = C::S;
-    const int ox = (q % a.tiles_x) * C::TX, oy = (q / a.tiles_x) * C::TY;
+    const int ox = (q % a.tiles_x) * C::TX, oy = (SLAB ? a.row_lo : 0) + (q / a.tiles_x) * C::TY;
     fence_proxy_async();
     mbar_expect_tx(L::bar(), C::TX_BYTES);
     tma_load_2d(L::stx(), tm_in, ox - S, oy - S, L::bar());
@@ -307,7 +307,7 @@ __device__ __forceinline__ void tile_dispatch(int h, TileRegs<K>& R, const doubl
 
 // One pass (h sub-sweeps, h <= S) over every tile this CTA owns.  If
 // `first_issued`, the TMA for this CTA's first tile is already in flight.
-template <int K>
+template <int K, bool SLAB>
 __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm_in,
                                           const CUtensorMap* tm_b, double* __restrict__ xout,
                                           int k0, int h, double (&acc)[tb2d::Cfg<K>::S],
@@ -321,13 +321,17 @@ __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm
     const int nx = a.g.nx, ny = a.g.ny;
     const double coff = a.g.c_off;
     if ((int)blockIdx.x >= a.ntiles) return;
-    if (threadIdx.x == 0 && !first_issued) tb2d_issue<K>(a, tm_in, tm_b, blockIdx.x);
+    if (threadIdx.x == 0 && !first_issued) tb2d_issue<K, SLAB>(a, tm_in, tm_b, blockIdx.x);
     for (int q = blockIdx.x; q < a.ntiles; q += gridDim.x) {
-        const int ox = (q % a.tiles_x) * C::TX, oy = (q / a.tiles_x) * C::TY;
+        const int ox = (q % a.tiles_x) * C::TX, oy = (SLAB ? a.row_lo : 0) + (q / a.tiles_x) * C::TY;
         const int gx0 = ox - S + c0;
         const int gy0 = oy - S + r0;
-        const bool masked = ox < S || oy < S || ox + C::TX + S > nx || oy + C::TY + S > ny;
+        // slab: a tile crossing row_hi reaches into ghost rows (updated, not owned)
+        const bool crosses = SLAB && oy + C::TY > a.row_hi;
+        const bool masked = ox < S || oy < S || ox + C::TX + S > nx || oy + C::TY + S > ny ||
+                            crosses;
         unsigned inmask = 0xffffffffu;
+        unsigned storemask = ownmask;
         if (masked) {
             inmask = 0u;
 #pragma unroll
@@ -336,8 +340,13 @@ __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm
                 for (int j = 0; j < CW; ++j)
                     if (gy0 + v >= 0 && gy0 + v < ny && gx0 + j >= 0 && gx0 + j < nx)
                         inmask |= 1u << (v * CW + j);
+            storemask &= inmask;
+            if (crosses) {  // rows >= row_hi are ghost rows: updated, not owned
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                    if (gy0 + v >= a.row_hi) storemask &= ~(((1u << CW) - 1u) << (v * CW));
+            }
         }
-        const unsigned storemask = ownmask & inmask;
         const unsigned accmask = accumulate ? storemask : 0u;
         mbar_wait(L::bar(), phase);
         phase ^= 1u;
@@ -353,7 +362,7 @@ __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm
         sts_cols<CW>(L::bot(0) + (warp + 1) * RX + c0, R.p[V - 1]);
         __syncthreads();  // stage consumed, halo rows published
         if (threadIdx.x == 0 && q + (int)gridDim.x < a.ntiles)
-            tb2d_issue<K>(a, tm_in, tm_b, q + gridDim.x);
+            tb2d_issue<K, SLAB>(a, tm_in, tm_b, q + gridDim.x);
         if (masked)
             tile_dispatch<K, true>(h, R, a.omegas + k0, a.g, warp, lane, inmask, accmask, acc, na);
         else
@@ -380,7 +389,7 @@ __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm
     }
 }
 
-template <int K>
+template <int K, bool SLAB>
 __global__ void __launch_bounds__(tb2d::Cfg<K>::THREADS, 1) __maxnreg__(tb2d::Cfg<K>::MAXREG)
     k_tb2d_cycle(const __grid_constant__ CUtensorMap tm_x0,
                  const __grid_constant__ CUtensorMap tm_x1,
@@ -412,13 +421,13 @@ __global__ void __launch_bounds__(tb2d::Cfg<K>::THREADS, 1) __maxnreg__(tb2d::Cf
     }
     uint32_t phase = 0, na = 0;
     const CUtensorMap* const tmx[2] = {&tm_x0, &tm_x1};
-    tb_run_cycle<S, F2D>(
+    tb_run_cycle<S, F2D, SLAB>(
         a, (int)blockIdx.x < a.ntiles,
         [&](int in, double* xout, int k0, int h, double (&acc)[S], bool accumulate, bool first) {
-            tb2d_pass<K>(a, tmx[in], &tm_b, xout, k0, h, acc, accumulate, ownmask, phase, first,
+            tb2d_pass<K, SLAB>(a, tmx[in], &tm_b, xout, k0, h, acc, accumulate, ownmask, phase, first,
                          na);
         },
-        [&](int in) { tb2d_issue<K>(a, tmx[in], &tm_b, blockIdx.x); },
+        [&](int in) { tb2d_issue<K, SLAB>(a, tmx[in], &tm_b, blockIdx.x); },
         [&]() {
             mbar_wait(L::bar(), phase);
             phase ^= 1u;
@@ -432,11 +441,14 @@ __global__ void __launch_bounds__(tb2d::Cfg<K>::THREADS, 1) __maxnreg__(tb2d::Cf
 template <int K>
 static cudaError_t setup_variant(int& per_sm) {
     using C = tb2d::Cfg<K>;
-    cudaError_t e = cudaFuncSetAttribute(k_tb2d_cycle<K>,
+    cudaError_t e = cudaFuncSetAttribute(k_tb2d_cycle<K, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tb2d_cycle<K>, C::THREADS,
-                                                         C::SMEM);
+    e = cudaFuncSetAttribute(k_tb2d_cycle<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tb2d_cycle<K, false>,
+                                                         C::THREADS, C::SMEM);
 }
 
 template <int K>
@@ -485,16 +497,19 @@ static cudaError_t launch_variant(const TbPlan& plan, const Geom& g, TbArgs& a, 
     if ((e = encode_field_map(&m1, x_alt, g.nx, g.ny, C::RX, C::RY)) != cudaSuccess) return e;
     if ((e = encode_field_map(&mb, b, g.nx, g.ny, C::RX, C::RY)) != cudaSuccess) return e;
     a.tiles_x = plan.tiles_x[K];
-    a.ntiles = plan.ntiles[K];
+    a.ntiles = a.tiles_x * ((a.row_hi - a.row_lo + C::TY - 1) / C::TY);
+    const int blocks = std::max(1, std::min(plan.blocks[K], a.ntiles));
     void* args[] = {&m0, &m1, &mb, &a};
-    return cudaLaunchCooperativeKernel((const void*)k_tb2d_cycle<K>, dim3(plan.blocks[K]),
-                                       dim3(C::THREADS), args, C::SMEM, st);
+    const void* kern = a.sums != nullptr ? (const void*)k_tb2d_cycle<K, true>
+                                         : (const void*)k_tb2d_cycle<K, false>;
+    return cudaLaunchCooperativeKernel(kern, dim3(blocks), dim3(C::THREADS), args, C::SMEM, st);
 }
 
 cudaError_t tb_launch_cycle(const TbPlan& plan, const Geom& g, double* x, double* x_alt,
                             const double* b, const double* omegas, int M, int s, double tol,
                             double baseline, double* partials, double* hist, int* out_i,
-                            double* out_d, cudaStream_t st) {
+                            double* out_d, cudaStream_t st, int row_lo, int row_hi,
+                            double* sums) {
     if ((((uintptr_t)x | (uintptr_t)x_alt | (uintptr_t)b) & 15) != 0)
         return cudaErrorMisalignedAddress;
     TbArgs a;
@@ -504,6 +519,9 @@ cudaError_t tb_launch_cycle(const TbPlan& plan, const Geom& g, double* x, double
     a.b = b;
     a.omegas = omegas;
     a.M = M;
+    a.row_lo = row_lo;
+    a.row_hi = row_hi;
+    a.sums = sums;
     const int k = tb_variant_for(plan, s);
     a.s = std::max(1, std::min(s, k == 1 ? tb2d::Cfg<1>::S : tb2d::Cfg<0>::S));
     a.tol = tol;

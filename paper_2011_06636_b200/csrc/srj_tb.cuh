@@ -31,10 +31,14 @@ int tb_variant_for(const TbPlan& plan, int s);
 // outputs as the one-sweep cycle kernel: out_i = {executed, status, result
 // buffer (0: x, 1: x_alt)}, out_d = {final sum of squares, res_after};
 // hist[k] = relative residual of x_k for k = 1..executed.
+// row_lo/row_hi: owned rows (slab with deep ghost rows; default the whole
+// grid); sums != nullptr: pass mode (one pass of M <= s sweeps, raw owned
+// sums of r^2 per sweep, no stop test, no residual tail; see srj_tbdriver.cuh).
 cudaError_t tb_launch_cycle(const TbPlan& plan, const Geom& g, double* x, double* x_alt,
                             const double* b, const double* omegas, int M, int s, double tol,
                             double baseline, double* partials, double* hist, int* out_i,
-                            double* out_d, cudaStream_t st);
+                            double* out_d, cudaStream_t st, int row_lo, int row_hi,
+                            double* sums);
 
 // 3D 7-point temporal blocking (srj_tb3d.cu): S = sweeps fused per pass.
 struct Tb3Plan {
@@ -67,6 +71,7 @@ void tbv_plan_free(TbvPlan& plan);
 cudaError_t tbv_launch_cycle(const TbvPlan& plan, const Geom& g, double* x, double* x_alt,
                              const double* b, const double* omegas, int M, int s, double tol,
                              double baseline, double* partials, double* hist, int* out_i,
-                             double* out_d, cudaStream_t st);
+                             double* out_d, cudaStream_t st, int row_lo, int row_hi,
+                             double* sums);
 
 }  // namespace srj

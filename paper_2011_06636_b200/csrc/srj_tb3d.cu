@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) __maxnreg__(C::MAXREG)
     uint32_t ph = 0;
     const CUtensorMap* const tmx[2] = {&tm_x0, &tm_x1};
     // tiles load their own planes (tile prologue): no speculative first-tile load
-    tb_run_cycle<S, F3D>(
+    tb_run_cycle<S, F3D, false>(
         a, (int)blockIdx.x < a.ntiles,
         [&](int in, double* xout, int k0, int h, double (&acc)[S], bool accumulate, bool) {
             tb3_pass<C>(a, tmx[in], &tm_b, xout, k0, h, acc, accumulate, ownmask, ph);
@@ -414,6 +414,9 @@ static cudaError_t tb3_launch(const Tb3Plan& plan, const Geom& g, double* x, dou
     a.out_d = out_d;
     a.tiles_x = plan.tiles_x;
     a.ntiles = plan.ntiles;
+    a.row_lo = 0;
+    a.row_hi = g.ny;
+    a.sums = nullptr;
     void* args[] = {&m0, &m1, &mb, &a};
     return cudaLaunchCooperativeKernel((const void*)k_tb3d_cycle<C>, dim3(plan.blocks),
                                        dim3(C::THREADS), args, C::SMEM, st);

@@ -32,6 +32,13 @@ struct TbArgs {
     int* out_i;
     double* out_d;
     int tiles_x, ntiles;
+    // Owned rows [row_lo, row_hi) (2D): tiles cover these rows; rows outside
+    // them but inside the grid are updated as ring points, never stored or
+    // accumulated (slab with deep ghost rows).  Whole grid: 0, ny.
+    int row_lo, row_hi;
+    // Pass mode (slab kernels): one pass of M <= s sweeps, no stop test and no
+    // residual tail; sums[t] = owned sum of r^2 of sub-sweep t (fixed order).
+    double* sums;
 };
 
 // pass(in, xout, k0, h, acc, accumulate, first_issued): one pass of h
@@ -40,7 +47,8 @@ struct TbArgs {
 // issue(in): (thread 0) start the TMA of this CTA's first tile of buffer `in`.
 // drain(): every thread waits for the outstanding TMA.
 // has_tiles: this CTA owns at least one tile.
-template <int S, int FAM, class Pass, class Issue, class Drain>
+// SLAB: pass mode (the slab instantiation of a kernel; see TbArgs::sums).
+template <int S, int FAM, bool SLAB, class Pass, class Issue, class Drain>
 __device__ __forceinline__ void tb_run_cycle(const TbArgs& a, bool has_tiles, Pass&& pass,
                                              Issue&& issue, Drain&& drain) {
     __shared__ double sh[32 * S];
@@ -64,6 +72,16 @@ __device__ __forceinline__ void tb_run_cycle(const TbArgs& a, bool has_tiles, Pa
         block_sums<S>(acc, h, sh, red);
         if (threadIdx.x < h) part[threadIdx.x * nb + blockIdx.x] = red[threadIdx.x];
         grid_barrier();
+        if constexpr (SLAB) {  // pass mode: raw sums, no decision, no tail
+            reduce_partials_multi(part, nb, h, red);
+            if (blockIdx.x == 0 && threadIdx.x < h) a.sums[threadIdx.x] = red[threadIdx.x];
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                a.out_i[0] = h;
+                a.out_i[1] = kStatusRan;
+                a.out_i[2] = (p + 1) & 1;
+            }
+            return;
+        }
         // Speculatively start the next pass's first tile while the stop test runs.
         if (p + 1 < npasses && has_tiles) {
             if (threadIdx.x == 0) issue((p + 1) & 1);

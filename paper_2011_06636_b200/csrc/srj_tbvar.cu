@@ -97,11 +97,13 @@ __device__ __forceinline__ void fma_sq_ifv(double& acc, double r, unsigned cond)
         : "d"(r), "r"(cond));
 }
 
+template <bool SLAB>
 __device__ __forceinline__ void tbv_issue(const TbvArgs& a, const CUtensorMap* tm_in,
                                           const TbvMaps& m, int q) {
     using C = tbv::Cfg;
     using L = TbvLayout;
-    const int ox = (q % a.tiles_x) * C::TX - C::S, oy = (q / a.tiles_x) * C::TY - C::S;
+    const int ox = (q % a.tiles_x) * C::TX - C::S,
+              oy = (SLAB ? a.row_lo : 0) + (q / a.tiles_x) * C::TY - C::S;
     fence_proxy_async();
     mbar_expect_tx(L::bar(), C::TX_BYTES);
     tma_load_2d(L::st(0), tm_in, ox, oy, L::bar());
@@ -227,6 +229,7 @@ __device__ __forceinline__ void tbv_dispatch(int h, TbvRegs& R, const double* om
     }
 }
 
+template <bool SLAB>
 __device__ __forceinline__ void tbv_pass(const TbvArgs& a, const CUtensorMap* tm_in,
                                          const TbvMaps& m, double* __restrict__ xout, int k0,
                                          int h, double (&acc)[tbv::Cfg::S], bool accumulate,
@@ -239,13 +242,17 @@ __device__ __forceinline__ void tbv_pass(const TbvArgs& a, const CUtensorMap* tm
     const int c0 = lane * CW, r0 = warp * V;
     const int nx = a.g.nx, ny = a.g.ny;
     if ((int)blockIdx.x >= a.ntiles) return;
-    if (threadIdx.x == 0 && !first_issued) tbv_issue(a, tm_in, m, blockIdx.x);
+    if (threadIdx.x == 0 && !first_issued) tbv_issue<SLAB>(a, tm_in, m, blockIdx.x);
     for (int q = blockIdx.x; q < a.ntiles; q += gridDim.x) {
-        const int ox = (q % a.tiles_x) * C::TX, oy = (q / a.tiles_x) * C::TY;
+        const int ox = (q % a.tiles_x) * C::TX, oy = (SLAB ? a.row_lo : 0) + (q / a.tiles_x) * C::TY;
         const int gx0 = ox - S + c0;
         const int gy0 = oy - S + r0;
-        const bool masked = ox < S || oy < S || ox + C::TX + S > nx || oy + C::TY + S > ny;
+        // slab: a tile crossing row_hi reaches into ghost rows (updated, not owned)
+        const bool crosses = SLAB && oy + C::TY > a.row_hi;
+        const bool masked = ox < S || oy < S || ox + C::TX + S > nx || oy + C::TY + S > ny ||
+                            crosses;
         unsigned inmask = 0xffffffffu;
+        unsigned storemask = ownmask;
         if (masked) {
             inmask = 0u;
 #pragma unroll
@@ -254,8 +261,13 @@ __device__ __forceinline__ void tbv_pass(const TbvArgs& a, const CUtensorMap* tm
                 for (int j = 0; j < CW; ++j)
                     if (gy0 + v >= 0 && gy0 + v < ny && gx0 + j >= 0 && gx0 + j < nx)
                         inmask |= 1u << (v * CW + j);
+            storemask &= inmask;
+            if (crosses) {  // rows >= row_hi are ghost rows: updated, not owned
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                    if (gy0 + v >= a.row_hi) storemask &= ~(((1u << CW) - 1u) << (v * CW));
+            }
         }
-        const unsigned storemask = ownmask & inmask;
         const unsigned accmask = accumulate ? storemask : 0u;
         mbar_wait(L::bar(), phase);
         phase ^= 1u;
@@ -277,7 +289,7 @@ __device__ __forceinline__ void tbv_pass(const TbvArgs& a, const CUtensorMap* tm
         __syncthreads();  // stages consumed, edge rows published
         ld2(R.cn, L::cse() + (warp + 2) * RX + c0);
         if (threadIdx.x == 0 && q + (int)gridDim.x < a.ntiles)
-            tbv_issue(a, tm_in, m, q + gridDim.x);
+            tbv_issue<SLAB>(a, tm_in, m, q + gridDim.x);
         if (masked)
             tbv_dispatch<true>(h, R, a.omegas + k0, warp, lane, inmask, accmask, acc, na);
         else
@@ -300,6 +312,7 @@ __device__ __forceinline__ void tbv_pass(const TbvArgs& a, const CUtensorMap* tm
     }
 }
 
+template <bool SLAB>
 __global__ void __launch_bounds__(tbv::Cfg::THREADS, 1)
     k_tbvar_cycle(const __grid_constant__ TbvMaps m, TbvArgs a) {
     using C = tbv::Cfg;
@@ -330,12 +343,12 @@ __global__ void __launch_bounds__(tbv::Cfg::THREADS, 1)
     }
     uint32_t phase = 0, na = 0;
     const CUtensorMap* const tmx[2] = {&m.x0, &m.x1};
-    tb_run_cycle<S, F2DV>(
+    tb_run_cycle<S, F2DV, SLAB>(
         a, (int)blockIdx.x < a.ntiles,
         [&](int in, double* xout, int k0, int h, double (&acc)[S], bool accumulate, bool first) {
-            tbv_pass(a, tmx[in], m, xout, k0, h, acc, accumulate, ownmask, phase, first, na);
+            tbv_pass<SLAB>(a, tmx[in], m, xout, k0, h, acc, accumulate, ownmask, phase, first, na);
         },
-        [&](int in) { tbv_issue(a, tmx[in], m, blockIdx.x); },
+        [&](int in) { tbv_issue<SLAB>(a, tmx[in], m, blockIdx.x); },
         [&]() {
             mbar_wait(L::bar(), phase);
             phase ^= 1u;
@@ -365,12 +378,15 @@ cudaError_t tbv_plan_init(TbvPlan& plan, const Geom& g, int num_sms) {
     plan = TbvPlan();
     // TMA needs 16-byte row pitches: even nx (x, b, fy, inv; fx via a padded copy).
     if (g.fam != F2DV || (g.nx & 1) || !g.fx || !g.fy || !tma_available()) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(k_tbvar_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_tbvar_cycle<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_tbvar_cycle<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tbvar_cycle, C::THREADS,
-                                                           C::SMEM)) != cudaSuccess)
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tbvar_cycle<false>,
+                                                           C::THREADS, C::SMEM)) != cudaSuccess)
         return e;
     if (per_sm < 1) return cudaSuccess;
     const size_t n = (size_t)g.nx * g.ny;
@@ -402,7 +418,8 @@ void tbv_plan_free(TbvPlan& plan) {
 cudaError_t tbv_launch_cycle(const TbvPlan& plan, const Geom& g, double* x, double* x_alt,
                              const double* b, const double* omegas, int M, int s, double tol,
                              double baseline, double* partials, double* hist, int* out_i,
-                             double* out_d, cudaStream_t st) {
+                             double* out_d, cudaStream_t st, int row_lo, int row_hi,
+                             double* sums) {
     using C = tbv::Cfg;
     if ((((uintptr_t)x | (uintptr_t)x_alt | (uintptr_t)b) & 15) != 0)
         return cudaErrorMisalignedAddress;
@@ -430,11 +447,16 @@ cudaError_t tbv_launch_cycle(const TbvPlan& plan, const Geom& g, double* x, doub
     a.hist = hist;
     a.out_i = out_i;
     a.out_d = out_d;
+    a.row_lo = row_lo;
+    a.row_hi = row_hi;
+    a.sums = sums;
     a.tiles_x = plan.tiles_x;
-    a.ntiles = plan.ntiles;
+    a.ntiles = a.tiles_x * ((row_hi - row_lo + C::TY - 1) / C::TY);
+    const int blocks = std::max(1, std::min(plan.blocks, a.ntiles));
     void* args[] = {&m, &a};
-    return cudaLaunchCooperativeKernel((const void*)k_tbvar_cycle, dim3(plan.blocks),
-                                       dim3(C::THREADS), args, C::SMEM, st);
+    const void* kern = sums != nullptr ? (const void*)k_tbvar_cycle<true>
+                                       : (const void*)k_tbvar_cycle<false>;
+    return cudaLaunchCooperativeKernel(kern, dim3(blocks), dim3(C::THREADS), args, C::SMEM, st);
 }
 
 }  // namespace srj

@@ -430,5 +430,234 @@ def local_slabs(family: str, shape, world: int, ranks, device, face_x=None, face
     return [Slab(layout, r, device, dx2=dx2, face_x=face_x, face_y=face_y) for r in ranks]
 
 
+# ---------------------------------------------------------------------------
+# Temporally blocked row slabs (2D): deep ghost rows, one exchange per pass
+# ---------------------------------------------------------------------------
+
+TB_GHOST = 6  # ghost rows per interior side = sweeps per pass (srj_tb_pass)
+
+
+class TbSlab:
+    """A 2D row slab extended by TB_GHOST ghost rows toward each neighbour (none
+    on a Dirichlet face).  Its operator covers the extended rows -- faces, b
+    and the iterate of the ghost rows included -- so one srj_tb_pass of up to
+    TB_GHOST sweeps updates the ghost rows as ring points and stores the owned
+    rows exactly as the single-GPU solve would."""
+
+    def __init__(self, layout: SlabLayout, rank: int, device, dx2: float | None = None,
+                 face_x=None, face_y=None):
+        if layout.family not in ("2d5", "2d5var"):
+            raise ValueError("temporally blocked slabs are 2D row slabs")
+        self.layout = layout
+        self.rank = rank
+        self.start, self.count = layout.span(rank)
+        nx = layout.shape[0]
+        g = TB_GHOST
+        self.g_lo = g if rank > 0 else 0
+        self.g_hi = g if rank < layout.world - 1 else 0
+        rows = self.count + self.g_lo + self.g_hi
+        r0 = self.start - self.g_lo  # global row of extended row 0
+        if layout.family == "2d5var":
+            fx = np.ascontiguousarray(face_x[r0:r0 + rows, :])
+            fy = np.ascontiguousarray(face_y[r0:r0 + rows + 1, :])
+            self.A = StencilOperator("2d5var", (nx, rows), face_x=fx, face_y=fy, device=device)
+        else:
+            if dx2 is None:
+                dx2 = (nx + 1.0) ** 2
+            self.A = StencilOperator("2d5", (nx, rows), dx2=dx2, device=device)
+        if not self.A.describe()["tb_supported"]:
+            raise ValueError("no temporally blocked kernel for this grid (odd nx?)")
+        self.device = device
+        self.nx = nx
+        self.row0 = r0
+        self.x = self.A.new_field()
+        self.x_alt = self.A.new_field()
+        self.snap = self.A.new_field()
+        self.b = self.A.new_field()
+
+    @property
+    def offset(self) -> int:
+        """Global flat index of the slab's first OWNED point."""
+        return self.start * self.nx
+
+    @property
+    def owned(self) -> tuple[int, int]:
+        return self.g_lo, self.g_lo + self.count
+
+    def rows(self, field: Field, r0: int, r1: int):
+        """View of extended rows [r0, r1) of a Field."""
+        h = field.halo
+        return field.buf[h + r0 * self.nx:h + r1 * self.nx]
+
+    def interior(self, field: Field):
+        lo, hi = self.owned
+        return self.rows(field, lo, hi)
+
+    def swap(self) -> None:
+        self.x, self.x_alt = self.x_alt, self.x
+
+
+class LocalTbExchanger(LocalExchanger):
+    """Virtual ranks in one process: deep ghost rows by device copies."""
+
+    def start_rows(self, slabs, fields):
+        g = TB_GHOST
+        for lo, hi, flo, fhi in zip(slabs[:-1], slabs[1:], fields[:-1], fields[1:]):
+            a, b = lo.owned
+            c, d = hi.owned
+            hi.rows(fhi, 0, g).copy_(lo.rows(flo, b - g, b))        # lo's last owned rows
+            lo.rows(flo, b, b + g).copy_(hi.rows(fhi, c, c + g))    # hi's first owned rows
+        return None
+
+
+class TorchTbExchanger(TorchExchanger):
+    """One slab per process: deep ghost rows over torch.distributed P2P."""
+
+    def start_rows(self, slabs, fields):
+        (s,), (f,) = slabs, fields
+        dist = self.dist
+        g = TB_GHOST
+        a, b = s.owned
+        ops = []
+        if self.rank > 0:
+            ops.append(dist.P2POp(dist.isend, s.rows(f, a, a + g), self.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, s.rows(f, 0, g), self.rank - 1, self.group))
+        if self.rank < self.world - 1:
+            ops.append(dist.P2POp(dist.isend, s.rows(f, b - g, b), self.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, s.rows(f, b, b + g), self.rank + 1, self.group))
+        return dist.batch_isend_irecv(ops) if ops else []
+
+
+class TbSlabSolver(SlabSolver):
+    """`solve` over temporally blocked row slabs: per cycle, passes of up to
+    TB_GHOST sweeps, each one deep ghost-row exchange plus one srj_tb_pass;
+    the residual of x_M over the owned rows; one all-gather of the per-sweep
+    owned sums; the same stop / rollback protocol as SlabSolver."""
+
+    def __init__(self, slabs: list[TbSlab], exchanger):
+        super().__init__(slabs, exchanger, engine=None)
+        if any(s.count < TB_GHOST for s in slabs):
+            raise ValueError(f"every slab needs at least {TB_GHOST} rows")
+        self._omega_cache = {}
+
+    # -- data ---------------------------------------------------------------
+    def load(self, b=None, x0=None, seed: int | None = None) -> None:
+        """As SlabSolver.load; b covers the extended rows (ghost rows hold the
+        neighbours' b, which never changes)."""
+        for s in self.slabs:
+            n_ext = s.A.n
+            lo = s.row0 * s.nx
+            if b is not None:
+                s.b.copy_(np.asarray(b)[lo:lo + n_ext])
+            elif seed is not None:
+                fill_uniform_rhs(s.b, seed, start=lo)
+            else:
+                raise ValueError("need b or seed")
+            s.x.buf.zero_()
+            s.x_alt.buf.zero_()
+            if x0 is not None:
+                s.x.copy_(np.asarray(x0)[lo:lo + n_ext])
+
+    def _padded_interior(self, s: TbSlab):
+        torch = _torch()
+        base, extra = divmod(self.layout.planes, self.layout.world)
+        size = (base + (1 if extra else 0)) * self.layout.plane_points
+        out = torch.zeros(size, dtype=torch.float64, device=s.x.buf.device)
+        out[:s.count * s.nx].copy_(s.interior(s.x))
+        return out
+
+    # -- kernels over all local slabs ----------------------------------------
+    def _exchange_rows(self) -> None:
+        self.ex.finish(self.ex.start_rows(self.slabs, [s.x for s in self.slabs]))
+
+    def _omegas(self, ordered):
+        torch = _torch()
+        key = tuple(ordered)
+        t = self._omega_cache.get(key)
+        if t is None:
+            t = torch.tensor(key, dtype=torch.float64, device=self.slabs[0].x.buf.device)
+            self._omega_cache[key] = t
+        return t
+
+    def _passes(self, om, sums, k_end: int) -> None:
+        """Sweeps 0 .. k_end-1 of the cycle in passes of <= TB_GHOST."""
+        k = 0
+        while k < k_end:
+            h = min(TB_GHOST, k_end - k)
+            self._exchange_rows()
+            for s, sm in zip(self.slabs, sums):
+                lo, hi = s.owned
+                s.A.tb_pass(s.x, s.x_alt, s.b, om.data_ptr() + 8 * k, h, lo, hi,
+                            sm.data_ptr() + 8 * k)
+            for s in self.slabs:
+                s.swap()
+            k += h
+
+    def _residual_into(self, sums, k: int) -> None:
+        self._exchange_rows()
+        for s, sm in zip(self.slabs, sums):
+            lo, hi = s.owned
+            s.A.sweep_planes(s.x, None, s.b, 0.0, lo, hi, sm.data_ptr() + 8 * k, 0)
+
+    def _sums_buffer(self, K: int):
+        torch = _torch()
+        return [torch.zeros(K, dtype=torch.float64, device=s.x.buf.device) for s in self.slabs]
+
+    def _global(self, sums, K: int) -> np.ndarray:
+        g = self.ex.allgather(sums).cpu().numpy()  # [world, K]
+        acc = np.zeros(K)
+        for r in range(g.shape[0]):  # fixed rank order: identical bits on every rank
+            acc = acc + g[r, :K]
+        return acc
+
+    def residual_norm(self) -> float:
+        sums = self._sums_buffer(1)
+        self._residual_into(sums, 0)
+        return math.sqrt(self._global(sums, 1)[0])
+
+    def cycle(self, ordered_omegas, res_before: float, tol: float, baseline: float,
+              budget: int):
+        M = len(ordered_omegas)
+        if res_before <= tol:
+            return 0, "converged", res_before, []
+        Meff = min(M, max(budget, 0))
+        if Meff == 0:
+            return 0, "ran", res_before, []
+        om = self._omegas(ordered_omegas)
+        for s in self.slabs:
+            s.snap.buf.copy_(s.x.buf)
+        sums = self._sums_buffer(Meff + 1)
+        self._passes(om, sums, Meff)
+        self._residual_into(sums, Meff)
+        res = np.sqrt(self._global(sums, Meff + 1)) / baseline
+        stop, status = None, "ran"
+        for k in range(1, Meff + 1):
+            if not math.isfinite(res[k]):
+                stop, status = k, "diverged"
+                break
+            if res[k] <= tol:
+                stop, status = k, "converged"
+                break
+        executed = Meff if stop is None else stop
+        if executed < Meff:
+            # roll back: x_executed from the cycle-start snapshot
+            for s in self.slabs:
+                s.x.buf.copy_(s.snap.buf)
+            self._passes(om, self._sums_buffer(Meff + 1), executed)
+        return executed, status, float(res[executed]), [float(v) for v in res[1:executed + 1]]
+
+    def solve(self, *args, **kwargs) -> SolveReport:
+        rep = super().solve(*args, **kwargs)
+        rep.x = [s.interior(s.x) for s in self.slabs]
+        return rep
+
+
+def local_tb_slabs(family: str, shape, world: int, ranks, device, face_x=None, face_y=None,
+                   dx2: float | None = None) -> list[TbSlab]:
+    layout = SlabLayout(family, tuple(shape), world)
+    return [TbSlab(layout, r, device, dx2=dx2, face_x=face_x, face_y=face_y) for r in ranks]
+
+
 __all__ = ["SlabLayout", "Slab", "LocalExchanger", "TorchExchanger", "DeviceEngine",
-           "SlabSolver", "local_slabs", "PARTS", "ABSOLUTE_L2"]
+           "SlabSolver", "local_slabs", "PARTS", "ABSOLUTE_L2", "TB_GHOST", "TbSlab",
+           "LocalTbExchanger", "TorchTbExchanger", "TbSlabSolver", "local_tb_slabs"]

@@ -171,6 +171,16 @@ class DeviceOperator:
             int(z_begin), int(z_end), ctypes.c_void_p(partial_ptr), int(slot),
             _stream_handle(self.device)), "srj_sweep_planes")
 
+    def tb_pass(self, x: Field, x_alt: Field, b: Field, omegas_ptr: int, h: int, row_lo: int,
+                row_hi: int, sums_ptr: int) -> None:
+        """One temporally blocked pass (h <= 6 sweeps) storing only the owned rows
+        [row_lo, row_hi) into x_alt; owned sums of r^2 per sweep at `sums_ptr`
+        (device).  Rows outside are a slab's deep ghost rows (srj_tb_pass)."""
+        _lib.check(_lib.lib().srj_tb_pass(
+            self.handle, x.ptr, x_alt.ptr, b.ptr, ctypes.c_void_p(omegas_ptr), int(h),
+            int(row_lo), int(row_hi), ctypes.c_void_p(sums_ptr), _stream_handle(self.device)),
+            "srj_tb_pass")
+
     def matvec(self, x: Field):
         torch = _torch()
         y = torch.empty(self.n, dtype=torch.float64, device=self.device)
