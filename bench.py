@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--cycles", type=int, default=50, help="c5: heuristic cycles per step")
     ap.add_argument("--slabs", action="store_true",
                     help="c3/c4: use the slab solver even on one GPU (it is used for N > 1)")
+    ap.add_argument("--no-tb-slabs", action="store_true",
+                    help="2D slabs: one sweep per launch instead of temporally blocked passes")
     return ap.parse_args()
 
 
@@ -232,8 +234,9 @@ def run_slabs(args, rank, world, local):
     import torch.distributed as dist
 
     import paper_2011_06636_b200 as srj
-    from paper_2011_06636_b200.distributed import (LocalExchanger, SlabSolver, TorchExchanger,
-                                                   local_slabs)
+    from paper_2011_06636_b200.distributed import (TB_GHOST, LocalExchanger, LocalTbExchanger,
+                                                   SlabSolver, TbSlabSolver, TorchExchanger,
+                                                   TorchTbExchanger, local_slabs, local_tb_slabs)
     from paper_2011_06636_b200.problems import CONFIGS, gaussian_field, harmonic_faces
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
@@ -255,9 +258,17 @@ def run_slabs(args, rank, world, local):
             face_x, face_y = harmonic_faces(np.exp(gaussian_field(n, args.seed)), (n + 1.0) ** 2)
         rule = srj.StoppingRule("relative_l2", args.tol, 10**9)
         max_cycles = None
-    slabs = local_slabs(family, shape, world, [rank], dev, face_x=face_x, face_y=face_y)
-    ex = TorchExchanger() if world > 1 else LocalExchanger(1)
-    solver = SlabSolver(slabs, ex)
+    # 2D row slabs of at least TB_GHOST rows with an even row length run the
+    # temporally blocked pass kernel with deep ghost rows; otherwise (and in 3D)
+    # one sweep per launch with one-plane halos
+    tb = (family in ("2d5", "2d5var") and shape[0] % 2 == 0
+          and shape[-1] // world >= TB_GHOST and not args.no_tb_slabs)
+    if tb:
+        slabs = local_tb_slabs(family, shape, world, [rank], dev, face_x=face_x, face_y=face_y)
+        solver = TbSlabSolver(slabs, TorchTbExchanger() if world > 1 else LocalTbExchanger(1))
+    else:
+        slabs = local_slabs(family, shape, world, [rank], dev, face_x=face_x, face_y=face_y)
+        solver = SlabSolver(slabs, TorchExchanger() if world > 1 else LocalExchanger(1))
     ctrl = srj.Heuristic()
     stream = torch.cuda.current_stream(dev)
 
@@ -292,11 +303,12 @@ def run_slabs(args, rank, world, local):
     # e2e: each rank stages its slab's b and x0 from pinned host memory and reads
     # its slab of the solution back (H2D + D2H inside the timed region)
     s0 = slabs[0]
+    n_owned = s0.count * s0.nx if tb else s0.A.n  # TB slabs also hold ghost rows
     solver.load(seed=args.seed)
     b_host = torch.empty(s0.A.n, dtype=torch.float64, pin_memory=True)
     b_host.copy_(s0.b.interior)
     x0_host = torch.zeros(s0.A.n, dtype=torch.float64, pin_memory=True)
-    x_out = torch.empty(s0.A.n, dtype=torch.float64, pin_memory=True)
+    x_out = torch.empty(n_owned, dtype=torch.float64, pin_memory=True)
 
     def one_e2e():
         s0.b.copy_(b_host)
@@ -324,7 +336,7 @@ def run_slabs(args, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
     e2e_val = n_global * sum(e2e_sweeps) / (e2e_total * 1e-3) / 1e9
-    per_gpu_bytes = float(BYTES_PER_UPDATE[family]) * slabs[0].A.n * sum(sweeps)
+    per_gpu_bytes = float(BYTES_PER_UPDATE[family]) * n_owned * sum(sweeps)
     peak, peak_kind = measured_peak()
     achieved = per_gpu_bytes / (total_ms * 1e-3) / 1e9
     line = {
@@ -344,10 +356,12 @@ def run_slabs(args, rank, world, local):
                                   "NCCL halo P2P overlapped"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                     "kernel": ("srj::k_sweep3d" if family == "3d7" else "srj::k_sweep2d")
-                               + " (slab sweep, whole step incl. exchange)"},
+                     "kernel": ("srj::k_tbvar_cycle / k_tb2d_cycle slab passes (srj_tb_pass)"
+                                if tb else
+                                ("srj::k_sweep3d" if family == "3d7" else "srj::k_sweep2d")
+                                + " (slab sweep)") + ", whole step incl. exchange"},
         "e2e": {"value": e2e_val, "unit": "GLUP/s", "h2d_bytes_per_step": 16 * s0.A.n * world,
-                "d2h_bytes_per_step": 8 * s0.A.n * world,
+                "d2h_bytes_per_step": 8 * n_owned * world,
                 "ms_per_step": e2e_total / len(e2e_ms)},
         "clocks": clocks.summary(),
         "gpu_launches": int(sum(sweeps) * 3 + len(rep.cycles) * 2),
