@@ -1,0 +1,91 @@
+"""Seeded random shapes through every cycle kernel, bit for bit against the oracle.
+
+For each (family, seed): a random grid (tiny, odd, non-square, single-row,
+multi-tile), random coefficients / right-hand side / start vector, one cycle
+of random omegas with a random stop position (or none), on the kernel the
+operator selects -- and, for 2D, both temporal-blocking ring variants and the
+single-sweep kernel.  The iterate must equal the oracle's sweeps exactly and
+the residuals to 1e-12.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_sweeps(op, x, b, omegas, baseline):
+    xs, res = [x], []
+    for w in omegas:
+        r, s = op.residual(xs[-1], b)
+        res.append(math.sqrt(s) / baseline)
+        xs.append(op.update(xs[-1], r, w))
+    _, s = op.residual(xs[-1], b)
+    res.append(math.sqrt(s) / baseline)
+    return xs, res
+
+
+def _case(family, seed):
+    rng = np.random.default_rng(1000 * seed + {"1d3": 1, "2d5": 2, "2d5var": 3, "3d7": 4}[family])
+    if family == "1d3":
+        dims = (int(rng.integers(1, 3000)),)
+    elif family == "3d7":
+        dims = tuple(int(v) for v in rng.integers(1, 70, 3))
+    else:
+        nx = int(rng.choice([int(rng.integers(1, 40)), int(rng.integers(40, 300))]))
+        ny = int(rng.choice([1, int(rng.integers(1, 30)), int(rng.integers(30, 260))]))
+        dims = (nx, ny)
+    return rng, dims
+
+
+@pytest.mark.parametrize("seed", range(20))
+@pytest.mark.parametrize("family", ["1d3", "2d5", "2d5var", "3d7"])
+def test_random_shape_cycle_bitwise(family, seed):
+    import torch
+
+    import paper_2011_06636_b200 as srj
+    from oracle import srj_oracle as O
+    rng, dims = _case(family, seed)
+    dev = torch.device("cuda", 0)
+    n = int(np.prod(dims))
+    nx, ny, nz = (list(dims) + [1, 1])[:3]
+    if family == "2d5var":
+        fx = rng.uniform(0.5, 30.0, (ny, nx + 1))
+        fy = rng.uniform(0.5, 30.0, (ny + 1, nx))
+        make = lambda: srj.StencilOperator(family, dims, face_x=fx, face_y=fy, device=dev)
+        op = O.StencilCPU(family, nx, ny, 1, 0.0, fx, fy)
+    else:
+        dx2 = float(rng.uniform(1.0, 50.0))
+        make = lambda: srj.StencilOperator(family, dims, dx2=dx2, device=dev)
+        op = O.StencilCPU(family, nx, ny, nz, dx2)
+    b = rng.uniform(-1, 1, n)
+    x0 = rng.uniform(-1, 1, n)
+    M = int(rng.integers(1, 20))
+    omegas = rng.uniform(0.3, 2.8, M)
+    baseline = float(rng.uniform(0.5, 4.0))
+    xs, res = _oracle_sweeps(op, x0, b, omegas, baseline)
+    stop = int(rng.integers(1, M + 1)) if rng.random() < 0.6 else None
+    tol = 0.0 if stop is None else res[stop] * (1.0 + 1e-9)
+    if stop is not None and any(r <= tol * (1.0 + 1e-9) for r in res[:stop]):
+        stop, tol = None, 0.0
+    k = M if stop is None else stop
+    spps = [1, 4, 6] if family in ("2d5", "2d5var") else [None]
+    for spp in spps:
+        A = make()
+        if spp is not None:
+            A.set_sweeps_per_pass(spp)
+        om = torch.tensor(omegas, dtype=torch.float64, device=dev)
+        x = A.field(x0)
+        x_alt = A.new_field()
+        hist = np.zeros(M)
+        out = A.run_cycle(x, x_alt, A.field(b), om, M, tol, baseline, res[0], 10**9, hist)
+        tag = (dims, spp, A.describe()["cycle_kernel"], stop)
+        assert out.executed == k, tag
+        got = (x_alt if out.result_in_alt else x).interior.cpu().numpy()
+        assert np.array_equal(got, xs[k]), tag
+        np.testing.assert_allclose(hist[:k], res[1:k + 1], rtol=1e-12, err_msg=str(tag))
+        np.testing.assert_allclose(out.res_after, res[k], rtol=1e-12, err_msg=str(tag))
