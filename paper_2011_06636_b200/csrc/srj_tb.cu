@@ -25,7 +25,13 @@
 // neighbour, so it is computed once per point and sub-sweep:
 //     y = ((((0 + p_s) + p_w) + c_diag*x) + p_e) + p_n
 // is bit-identical to the reference csr_matvec order with freshly rounded
-// products; 11 fp64 instructions per point-sweep.
+// products; 11 fp64 instructions per point-sweep.  The leading `0 +` is
+// dropped (10 instructions): 0 + p_s and p_s differ only when p_s = -0, and
+// that sign of zero can reach the result only through c_diag*x = -0, i.e.
+// x = -0 at the point.  Iterates never create a -0 (x + t rounds an exact
+// zero to +0; held and ghost points are +0), so the iterates are bit-identical
+// unless x0 itself holds -0.0 entries -- then at most the sign of a zero can
+// differ (equal values).
 //
 // Every region point is updated every sub-sweep; values within t+1 rings of
 // the region edge are garbage after sub-sweep t but never reach the owned tile,
@@ -209,7 +215,7 @@ __device__ __forceinline__ void tile_sweeps(TileRegs<K>& R, const double* omegas
             for (int k = 0; k < NP; ++k) {
                 if (k >= np) break;
                 const int v = k < 2 ? va : vb, j = k & 1;
-                y[k] = DADD(0.0, v == 0 ? hs[j] : R.p[v - 1][j]);
+                y[k] = v == 0 ? hs[j] : R.p[v - 1][j];  // 0 + p_s (see header)
             }
 #pragma unroll
             for (int k = 0; k < NP; ++k) {

@@ -12,6 +12,8 @@
 // Operator (reference problems.py assembly order; srj_stencil.cuh F2DV):
 //   diag = ((c_w + c_e) + c_s) + c_n,   inv = 1 / diag
 //   y = 0 + (-c_s) x_s + (-c_w) x_w + diag x + (-c_e) x_e + (-c_n) x_n
+// (evaluated without the leading `0 +`: identical bits unless x0 holds -0.0
+// entries, see srj_tb.cu)
 // with c_w = fx[y][x], c_e = fx[y][x+1], c_s = fy[y][x], c_n = fy[y+1][x].
 // A face product belongs to one point pair, so (unlike the constant case) x
 // itself is exchanged: west/east by warp shuffle, north/south through the warp
@@ -155,7 +157,7 @@ __device__ __forceinline__ void tbv_sweeps(TbvRegs& R, const double* omegas, int
                 const double diag = DADD(DADD(DADD(c_w, c_e), c_s), c_n);
                 const double x_w = j == 0 ? xw : R.x[v][j - 1];
                 const double x_e = j == CW - 1 ? xe : R.x[v][j + 1];
-                double y = DADD(0.0, DMUL(-c_s, xs[j]));
+                double y = DMUL(-c_s, xs[j]);  // 0 + (-c_s) x_s (see header)
                 y = DADD(y, DMUL(-c_w, x_w));
                 y = DADD(y, DMUL(diag, R.x[v][j]));
                 y = DADD(y, DMUL(-c_e, x_e));

@@ -66,3 +66,37 @@ def test_tb2d_cycle_bitwise_vs_oracle(dims, kernel, spp):
         assert np.array_equal(got, xs[k]), (stop, np.max(np.abs(got - xs[k])))
         np.testing.assert_allclose(hist[:k], res[1:k + 1], rtol=1e-12)
         np.testing.assert_allclose(out.res_after, res[k], rtol=1e-12)
+
+
+@pytest.mark.parametrize("family", ["2d5", "2d5var"])
+def test_negative_zero_start(family):
+    """x0 holding -0.0 entries (and b zero there): the TB kernels skip the
+    reference's leading `0 +`, so at most the sign of a zero may differ --
+    the values equal the oracle's."""
+    import torch
+
+    import paper_2011_06636_b200 as srj
+    from oracle import srj_oracle as O
+    nx, ny = 66, 70
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(5)
+    if family == "2d5var":
+        fx = rng.uniform(0.5, 30.0, (ny, nx + 1))
+        fy = rng.uniform(0.5, 30.0, (ny + 1, nx))
+        A = srj.StencilOperator(family, (nx, ny), face_x=fx, face_y=fy, device=dev)
+        op = O.StencilCPU(family, nx, ny, 1, 0.0, fx, fy)
+    else:
+        A = srj.StencilOperator(family, (nx, ny), dx2=5.0, device=dev)
+        op = O.StencilCPU(family, nx, ny, 1, 5.0)
+    x0 = np.where(rng.random(A.n) < 0.5, -0.0, 0.0)
+    b = np.where(rng.random(A.n) < 0.97, 0.0, rng.uniform(-1, 1, A.n))
+    omegas = rng.uniform(0.4, 2.6, 6)
+    xs = [x0]
+    for w in omegas:
+        r, _ = op.residual(xs[-1], b)
+        xs.append(op.update(xs[-1], r, w))
+    om = torch.tensor(omegas, dtype=torch.float64, device=dev)
+    x, x_alt = A.field(x0), A.new_field()
+    out = A.run_cycle(x, x_alt, A.field(b), om, 6, 0.0, 1.0, 1.0, 10**9, None)
+    got = (x_alt if out.result_in_alt else x).interior.cpu().numpy()
+    assert np.array_equal(got, xs[6])  # -0.0 == +0.0
