@@ -240,6 +240,7 @@ class SlabSolver:
         self.engine = engine if engine is not None else DeviceEngine()
         self.layout = slabs[0].layout
         self._parts = None
+        self.launches = 0  # kernel launches issued by this solver (bench evidence)
 
     # -- data ---------------------------------------------------------------
     def load(self, b=None, x0=None, seed: int | None = None) -> None:
@@ -290,7 +291,8 @@ class SlabSolver:
     def _sweep(self, w: float, parts, k: int) -> None:
         eng = self.engine
         P = [s.planes for s in self.slabs]
-        if getattr(eng, "overlap", False) and min(P) >= 3:
+        # the interior/boundary split only pays when a halo exchange can overlap
+        if getattr(eng, "overlap", False) and min(P) >= 3 and self.layout.world > 1:
             handle = self.ex.start([s.x for s in self.slabs])
             for s, p in zip(self.slabs, parts):
                 eng.apply(s, s.x, s.x_alt, w, 1, s.planes - 1, p[k, 0], 0)
@@ -298,10 +300,12 @@ class SlabSolver:
             for s, p in zip(self.slabs, parts):
                 eng.apply(s, s.x, s.x_alt, w, 0, 1, p[k, 1], 1)
                 eng.apply(s, s.x, s.x_alt, w, s.planes - 1, s.planes, p[k, 2], 1)
+            self.launches += 3 * len(self.slabs)
         else:
             self.ex.exchange([s.x for s in self.slabs])
             for s, p in zip(self.slabs, parts):
                 eng.apply(s, s.x, s.x_alt, w, 0, s.planes, p[k, 0], 0)
+            self.launches += len(self.slabs)
         for s in self.slabs:
             s.swap()
 
@@ -309,6 +313,7 @@ class SlabSolver:
         self.ex.exchange([s.x for s in self.slabs])
         for s, p in zip(self.slabs, parts):
             self.engine.apply(s, s.x, None, 0.0, 0, s.planes, p[k, 0], 0)
+        self.launches += len(self.slabs)
 
     def _global_sums(self, parts, K: int) -> np.ndarray:
         g = self.ex.allgather(parts).cpu().numpy()  # [world, K, PARTS]
@@ -589,6 +594,7 @@ class TbSlabSolver(SlabSolver):
                 lo, hi = s.owned
                 s.A.tb_pass(s.x, s.x_alt, s.b, om.data_ptr() + 8 * k, h, lo, hi,
                             sm.data_ptr() + 8 * k)
+            self.launches += len(self.slabs)
             for s in self.slabs:
                 s.swap()
             k += h
@@ -598,6 +604,7 @@ class TbSlabSolver(SlabSolver):
         for s, sm in zip(self.slabs, sums):
             lo, hi = s.owned
             s.A.sweep_planes(s.x, None, s.b, 0.0, lo, hi, sm.data_ptr() + 8 * k, 0)
+        self.launches += len(self.slabs)
 
     def _sums_buffer(self, K: int):
         torch = _torch()
