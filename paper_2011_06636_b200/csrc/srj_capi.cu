@@ -167,11 +167,13 @@ __global__ void __launch_bounds__(kSmall1dThreads) k_small_cycle_1d(CycleArgs a)
     __syncthreads();
     int executed = a.M, status = kStatusRan, last = 0;
     double S = 0.0;
+    double w_next = a.M > 0 ? __ldg(a.omegas) : 0.0;  // loaded one sweep ahead
     for (int k = 0; k <= a.M; ++k) {
         const bool tail = (k == a.M);
         const int bi = (k & 1) ? base1 : base0;
         const int bo = (k & 1) ? base0 : base1;
-        const double w = tail ? 0.0 : __ldg(a.omegas + k);
+        const double w = w_next;
+        if (k + 1 < a.M) w_next = __ldg(a.omegas + k + 1);
         double acc = 0.0;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             const double xl = sm[bi + i - 1], xc = sm[bi + i], xr = sm[bi + i + 1];
@@ -202,6 +204,113 @@ __global__ void __launch_bounds__(kSmall1dThreads) k_small_cycle_1d(CycleArgs a)
         const int src = (executed & 1) ? base1 : base0;
         double* dst = (executed & 1) ? a.xb : const_cast<double*>(a.xa);
         for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = sm[src + i];
+    }
+    __syncthreads();  // thread 0's hist stores are visible to the CTA
+    for (int k = 1 + threadIdx.x; k <= last; k += blockDim.x) a.hist[k] = sqrt(a.hist[k]) / a.baseline;
+    if (threadIdx.x == 0) {
+        a.out_i[0] = executed;
+        a.out_i[1] = status;
+        a.out_i[2] = executed & 1;
+        a.out_d[0] = S;
+        a.out_d[1] = sqrt(S) / a.baseline;
+    }
+}
+
+// Register-resident 1D cycle (n <= 32 * kReg1dWarps * 16): 8 warps, lane l of
+// warp w holds P consecutive points [(32w + l) P, +P) -- x, b and p = c*x in
+// registers for the whole cycle.  Neighbours inside a lane are registers, across
+// lanes one shuffle each way, across warps the edge p of the neighbouring warps
+// through shared memory (double-buffered by sweep parity).  Per sweep: residual
+// r_k of x_k at every point, warp butterfly of r^2 into red[parity][warp],
+// x_{k+1} committed (x_k kept for a stop at k), edge p published, ONE
+// __syncthreads, then every warp reduces the 4 partials in warp order
+// (identical bits everywhere) and applies the stop test.  Points past n are
+// held at 0.  Same protocol and outputs as k_cycle.
+constexpr int kReg1dWarps = 8;
+
+template <int P>
+__global__ void __launch_bounds__(32 * kReg1dWarps) k_reg_cycle_1d(CycleArgs a) {
+    __shared__ double edge[2][2][kReg1dWarps + 2];  // [parity][first|last][warp + 1]
+    __shared__ double red[2][kReg1dWarps];
+    const int n = a.g.nx;
+    const double c = a.g.c_off, d = a.g.c_diag, inv = a.g.inv_diag;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int i0 = (wid * 32 + lane) * P;
+    double x[P], xo[P], b[P], p[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+        const bool in = i0 + j < n;
+        x[j] = in ? a.xa[i0 + j] : 0.0;
+        b[j] = in ? a.b[i0 + j] : 0.0;
+        p[j] = DMUL(c, x[j]);
+    }
+    const double pz = DMUL(c, 0.0);  // ghost / past-n neighbour: c*0 (a no-op term)
+    if (threadIdx.x < 2 * 2 * (kReg1dWarps + 2)) (&edge[0][0][0])[threadIdx.x] = pz;
+    __syncthreads();
+    if (lane == 0) edge[0][0][wid + 1] = p[0];
+    if (lane == 31) edge[0][1][wid + 1] = p[P - 1];
+    const double tb = a.tol * a.baseline;
+    const double hi2 = a.tol > 0.0 ? DMUL(DMUL(tb, tb), 1.0 + 1e-12) : -1.0;
+    __syncthreads();
+    int executed = a.M, status = kStatusRan, last = 0;
+    double S = 0.0;
+    bool have_old = false;
+    // omega of the next sweep is loaded one sweep ahead (its L2 latency would
+    // otherwise sit on every sweep's critical path)
+    double w_next = a.M > 0 ? __ldg(a.omegas) : 0.0;
+    for (int k = 0; k <= a.M; ++k) {
+        const bool tail = (k == a.M);
+        const int par = k & 1;
+        const double w = w_next;
+        if (k + 1 < a.M) w_next = __ldg(a.omegas + k + 1);
+        // neighbours across the lane / warp boundaries (old p)
+        double pl = __shfl_up_sync(0xffffffffu, p[P - 1], 1);
+        double pr = __shfl_down_sync(0xffffffffu, p[0], 1);
+        if (lane == 0) pl = edge[par][1][wid];       // last point of warp-1
+        if (lane == 31) pr = edge[par][0][wid + 2];  // first point of warp+1
+        double r[P], acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            double y = DADD(0.0, j == 0 ? pl : p[j - 1]);
+            y = DADD(y, DMUL(d, x[j]));
+            y = DADD(y, j == P - 1 ? pr : p[j + 1]);
+            r[j] = DSUB(b[j], y);
+            if (i0 + j < n) acc = fma(r[j], r[j], acc);
+        }
+        acc = warp_allsum(acc);
+        if (lane == 0) red[par][wid] = acc;
+        if (!tail) {
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                xo[j] = x[j];
+                x[j] = i0 + j < n ? relax(x[j], inv, r[j], w) : 0.0;
+                p[j] = DMUL(c, x[j]);
+            }
+            have_old = true;
+            if (lane == 0) edge[par ^ 1][0][wid + 1] = p[0];
+            if (lane == 31) edge[par ^ 1][1][wid + 1] = p[P - 1];
+        }
+        __syncthreads();
+        S = red[par][0];
+#pragma unroll
+        for (int q = 1; q < kReg1dWarps; ++q) S = DADD(S, red[par][q]);
+        if (k >= 1) {
+            last = k;
+            if (threadIdx.x == 0) a.hist[k] = S;  // converted below
+            if (!(S > hi2 && S < 1e300)) {
+                const double res = sqrt(S) / a.baseline;
+                if (!isfinite(res)) { executed = k; status = kStatusDiverged; break; }
+                if (res <= a.tol) { executed = k; status = kStatusConverged; break; }
+            }
+        }
+    }
+    // x_executed: the committed x, or x_k (kept in xo) after a stop at k < M
+    const bool use_old = executed < a.M && have_old;
+    if (executed > 0) {
+        double* dst = (executed & 1) ? a.xb : const_cast<double*>(a.xa);
+#pragma unroll
+        for (int j = 0; j < P; ++j)
+            if (i0 + j < n) dst[i0 + j] = use_old ? xo[j] : x[j];
     }
     __syncthreads();  // thread 0's hist stores are visible to the CTA
     for (int k = 1 + threadIdx.x; k <= last; k += blockDim.x) a.hist[k] = sqrt(a.hist[k]) / a.baseline;
@@ -548,6 +657,7 @@ int srj_op_describe(const srj_op* op, srj_op_info* info) {
                             op->tb_kind == SRJ_TB_WARP_STREAM) ? SRJ_KERNEL_WS2D
                          : (op->sweeps_per_pass > 1 && op->tb.supported) ? SRJ_KERNEL_TB2D
                          : op->p2.supported                               ? SRJ_KERNEL_TILE2D
+                         : (op->g.fam == F1D && op->g.nx <= 32 * kReg1dWarps * 16) ? SRJ_KERNEL_REG1D
                          : (op->g.fam == F1D && op->g.nx <= kSmall1dMaxN) ? SRJ_KERNEL_SMALL1D
                                                                           : SRJ_KERNEL_GENERIC;
     return SRJ_OK;
@@ -577,6 +687,16 @@ static int launch_cycle(srj_op* op, const double* xa, double* xb, const double* 
     a.hist = op->hist;
     a.out_i = op->out_i;
     a.out_d = op->out_d;
+    if (!diff && op->g.fam == F1D && op->g.nx <= 32 * kReg1dWarps * 16) {
+        const int per = (op->g.nx + 32 * kReg1dWarps - 1) / (32 * kReg1dWarps);
+        const dim3 grid(1), block(32 * kReg1dWarps);
+        if (per <= 2) k_reg_cycle_1d<2><<<grid, block, 0, st>>>(a);
+        else if (per <= 4) k_reg_cycle_1d<4><<<grid, block, 0, st>>>(a);
+        else if (per <= 8) k_reg_cycle_1d<8><<<grid, block, 0, st>>>(a);
+        else k_reg_cycle_1d<16><<<grid, block, 0, st>>>(a);
+        CUDA_TRY(cudaGetLastError());
+        return SRJ_OK;
+    }
     if (!diff && op->g.fam == F1D && op->g.nx <= kSmall1dMaxN) {
         const size_t smem = (size_t)(3 * op->g.nx + 4) * sizeof(double);
         k_small_cycle_1d<<<1, kSmall1dThreads, smem, st>>>(a);

@@ -1,5 +1,6 @@
-"""1D cycle kernels vs the oracle: the single-CTA shared-memory kernel
-(n <= 8192, BASELINE config 1) and the generic row walker above it, swept
+"""1D cycle kernels vs the oracle: the single-CTA register-resident kernel
+(n <= 4096, BASELINE config 1), the single-CTA shared-memory kernel (n <= 8192)
+and the generic row walker above it, swept
 cycle by cycle with every stop position, plus a residual-only evaluation.
 The 1D golden solves (test_gpu_parity.py) already run through the small kernel.
 """
@@ -25,7 +26,9 @@ def _oracle_sweeps(op, x, b, omegas, baseline):
     return xs, res
 
 
-@pytest.mark.parametrize("n,kernel", [(1, 7), (1000, 7), (8192, 7), (8193, 0), (20000, 0)])
+@pytest.mark.parametrize("n,kernel", [(1, 8), (2, 8), (127, 8), (200, 8), (1000, 8), (1024, 8),
+                                      (2048, 8), (4096, 8), (4097, 7), (8192, 7), (8193, 0),
+                                      (20000, 0)])
 def test_1d_cycle_bitwise_vs_oracle(n, kernel):
     import torch
 
