@@ -1,6 +1,7 @@
 // Temporally blocked SRJ cycle for the 2D 5-point constant-coefficient
-// stencil (BASELINE config 2): S = 4 consecutive sweeps, each with its own
-// omega, per HBM/L2 round trip of x and b.
+// stencil (BASELINE config 2): up to S consecutive sweeps (S = 6 ring by
+// default, S = 4 for <= 4 sweeps per pass), each with its own omega, per
+// HBM/L2 round trip of x and b.
 //
 // Tiling.  A CTA (one per SM, persistent, cooperative launch) owns TX x TY
 // output tiles.  For each tile the copy engine (TMA) brings the RX x RY region
@@ -14,8 +15,9 @@
 // live in registers for all S sub-sweeps.  Neighbours:
 //   west/east  -- registers, or a warp shuffle across the lane boundary;
 //   north/south -- registers, or the halo rows the warps above/below publish
-//                  in shared memory (double-buffered by sub-sweep parity,
-//                  one __syncthreads per sub-sweep).
+//                  in shared memory (double-buffered by sub-sweep parity; a
+//                  split mbarrier per sub-sweep: interior rows are computed
+//                  between a warp's arrival and its wait).
 // Measured on B200 (tools/probe/rates_probe.cu): a 64-bit warp shuffle costs
 // ~1/3 of the shared-memory bandwidth an LDS.64 exchange needs, so the only
 // shared traffic left is the staging load and the halo rows.
@@ -39,11 +41,11 @@
 // iterates).  Grid-exterior points are held at 0.
 //
 // Residuals.  Sub-sweep t accumulates (b - A x_{k0+t})^2 over OWNED points
-// only.  After a pass a grid barrier lets every CTA reduce the per-CTA partials
-// in a fixed order and apply the reference's per-sweep stopping rule
-// (solver.py:216-222,235-239).  A stop at sweep k0+j, j >= 1, re-runs the pass
-// with j sub-sweeps from its intact input buffer (rollback); j = 0 returns the
-// input buffer itself.
+// only; the per-cycle driver (srj_tbdriver.cuh) reduces them after each pass,
+// applies the reference's per-sweep stopping rule (solver.py:216-222,235-239)
+// and rolls back a pass that stops inside.  The SLAB instantiation serves
+// srj_tb_pass: tiles cover the owned rows [row_lo, row_hi) of a row slab
+// whose deep ghost rows are updated as ring points but never stored.
 #include <cooperative_groups.h>
 
 #include <algorithm>
