@@ -576,10 +576,12 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
     }
     // Default: 6 fused sweeps per pass where a 2D temporally blocked kernel
     // exists (the S=6 rings measured fastest on B200 for constant and variable
-    // coefficients), else one per pass.  3D keeps the
-    // HBM-bound plane ring by default: the z-wavefront TB kernel (sweeps_per_pass
-    // 2) measured slower on B200.
-    op->sweeps_per_pass = (op->tb.supported || op->tbv.supported) ? 6 : op->ws.supported ? 4 : 1;
+    // coefficients), 2 for the 3D temporally blocked kernel (512^3 sweep: 296 us
+    // vs 603 for the HBM-bound plane ring), else one per pass.
+    op->sweeps_per_pass = (op->tb.supported || op->tbv.supported) ? 6
+                          : op->tb3.supported                     ? 2
+                          : op->ws.supported                      ? 4
+                                                                  : 1;
     op->slot_capacity = std::max(op->p3.slots, kApplyBlocksPerSm * op->num_sms);
     for (int s = 0; s < kSlots; ++s) {
         if ((e = cudaMalloc(&op->slot_part[s], op->slot_capacity * sizeof(double))) != cudaSuccess) {

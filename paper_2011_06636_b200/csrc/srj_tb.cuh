@@ -45,7 +45,7 @@ struct Tb3Plan {
     bool supported = false;
     int blocks = 0, tiles_x = 0, ntiles = 0;
     int sweeps = 0;
-    int variant = 0;  // tb3d::C<variant> (SRJ_TB3_VARIANT, tuning only)
+    int zc = 0, items = 0;  // planes per work item, work items (tiles x z-runs)
 };
 
 cudaError_t tb3_plan_init(Tb3Plan& plan, const Geom& g, int num_sms);

@@ -48,7 +48,9 @@ struct TbArgs {
 // drain(): every thread waits for the outstanding TMA.
 // has_tiles: this CTA owns at least one tile.
 // SLAB: pass mode (the slab instantiation of a kernel; see TbArgs::sums).
-template <int S, int FAM, bool SLAB, class Pass, class Issue, class Drain>
+// TAIL_PASS: the residual of the cycle's final iterate is a pass with h = 0
+// (xout == nullptr; acc[0] = owned sum of r^2) instead of the generic walker.
+template <int S, int FAM, bool SLAB, bool TAIL_PASS = false, class Pass, class Issue, class Drain>
 __device__ __forceinline__ void tb_run_cycle(const TbArgs& a, bool has_tiles, Pass&& pass,
                                              Issue&& issue, Drain&& drain) {
     __shared__ double sh[32 * S];
@@ -121,7 +123,16 @@ __device__ __forceinline__ void tb_run_cycle(const TbArgs& a, bool has_tiles, Pa
         // residual of the cycle's final iterate (solver.py:233-234,248-249)
         const int u0 = (int)((long long)a.g.units * blockIdx.x / nb);
         const int u1 = (int)((long long)a.g.units * (blockIdx.x + 1) / nb);
-        double acc = walk_units<FAM, kResid>(a.g, buf[result], nullptr, a.b, 0.0, u0, u1);
+        double acc;
+        if constexpr (TAIL_PASS) {
+            double t[S];
+#pragma unroll
+            for (int q = 0; q < S; ++q) t[q] = 0.0;
+            pass(result, nullptr, 0, 0, t, true, false);
+            acc = t[0];
+        } else {
+            acc = walk_units<FAM, kResid>(a.g, buf[result], nullptr, a.b, 0.0, u0, u1);
+        }
         double* part = a.partials + (size_t)(npasses & 1) * kTbMaxSub * nb;
         acc = block_allsum(acc, sh1);
         if (threadIdx.x == 0) part[blockIdx.x] = acc;
