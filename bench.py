@@ -67,7 +67,7 @@ def parse():
     ap.add_argument("--slabs", action="store_true",
                     help="c3/c4: use the slab solver even on one GPU (it is used for N > 1)")
     ap.add_argument("--no-tb-slabs", action="store_true",
-                    help="2D slabs: one sweep per launch instead of temporally blocked passes")
+                    help="slabs: one sweep per launch instead of temporally blocked passes")
     return ap.parse_args()
 
 
@@ -234,9 +234,10 @@ def run_slabs(args, rank, world, local):
     import torch.distributed as dist
 
     import paper_2011_06636_b200 as srj
-    from paper_2011_06636_b200.distributed import (TB_GHOST, LocalExchanger, LocalTbExchanger,
+    from paper_2011_06636_b200.distributed import (LocalExchanger, LocalTbExchanger,
                                                    SlabSolver, TbSlabSolver, TorchExchanger,
-                                                   TorchTbExchanger, local_slabs, local_tb_slabs)
+                                                   TorchTbExchanger, local_slabs, local_tb_slabs,
+                                                   tb_ghost)
     from paper_2011_06636_b200.problems import CONFIGS, gaussian_field, harmonic_faces
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
@@ -258,11 +259,11 @@ def run_slabs(args, rank, world, local):
             face_x, face_y = harmonic_faces(np.exp(gaussian_field(n, args.seed)), (n + 1.0) ** 2)
         rule = srj.StoppingRule("relative_l2", args.tol, 10**9)
         max_cycles = None
-    # 2D row slabs of at least TB_GHOST rows with an even row length run the
-    # temporally blocked pass kernel with deep ghost rows; otherwise (and in 3D)
-    # one sweep per launch with one-plane halos
-    tb = (family in ("2d5", "2d5var") and shape[0] % 2 == 0
-          and shape[-1] // world >= TB_GHOST and not args.no_tb_slabs)
+    # slabs of at least tb_ghost rows (planes) with an even row length run the
+    # temporally blocked pass kernel with deep ghost rows (2D: 6 rows, 3D: 2
+    # planes); otherwise one sweep per launch with one-plane halos
+    tb = (family in ("2d5", "2d5var", "3d7") and shape[0] % 2 == 0
+          and shape[-1] // world >= tb_ghost(family) and not args.no_tb_slabs)
     if tb:
         slabs = local_tb_slabs(family, shape, world, [rank], dev, face_x=face_x, face_y=face_y)
         solver = TbSlabSolver(slabs, TorchTbExchanger() if world > 1 else LocalTbExchanger(1))
@@ -354,11 +355,15 @@ def run_slabs(args, rank, world, local):
                    "levels": [c.level for c in rep.cycles],
                    "executed": [c.executed for c in rep.cycles],
                    "time_to_tolerance_ms": None if throughput else total_ms / args.steps,
-                   "parallelism": f"{'z' if family == '3d7' else 'row'}-slabs x{world}, "
-                                  "NCCL halo P2P overlapped"},
+                   "parallelism": f"{'z' if family == '3d7' else 'row'}-slabs x{world}, " + (
+                       f"deep NCCL halo P2P ({tb_ghost(family)} {'planes' if family == '3d7' else 'rows'}) "
+                       "per temporally blocked pass" if tb else
+                       "NCCL halo P2P overlapped with interior sweeps")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                     "kernel": ("srj::k_tbvar_cycle / k_tb2d_cycle slab passes (srj_tb_pass)"
+                     "kernel": (("srj::k_tb3d_cycle<true> slab passes (srj_tb_pass, 2 sweeps)"
+                                 if family == "3d7" else
+                                 "srj::k_tbvar_cycle / k_tb2d_cycle slab passes (srj_tb_pass)")
                                 if tb else
                                 ("srj::k_sweep3d" if family == "3d7" else "srj::k_sweep2d")
                                 + " (slab sweep)") + ", whole step incl. exchange"},

@@ -201,10 +201,11 @@ int64_t srj_op_planes(const srj_op* op);
 int srj_sweep_planes(srj_op* op, const double* x, double* x_out, const double* b,
                      double omega, int64_t z_begin, int64_t z_end, double* partial_dev,
                      int32_t slot, void* stream);
-/* Temporally blocked slab pass (2D constant or variable coefficient, even nx):
- * h <= 6 consecutive sweeps with omegas_dev[0..h-1] over the operator's grid,
- * storing only the owned rows [row_lo, row_hi) of x_alt (the rows outside are
- * the deep ghost rows of a slab: updated as ring points, never stored).
+/* Temporally blocked slab pass (2D constant or variable coefficient, or 3D
+ * 7-point; even nx): h consecutive sweeps (h <= 6 in 2D, <= 2 in 3D) with
+ * omegas_dev[0..h-1] over the operator's grid, storing only the owned rows
+ * (3D: z planes) [row_lo, row_hi) of x_alt (the rows outside are the deep
+ * ghost rows / planes of a slab: updated as ring points, never stored).
  * sums_dev[t] (device) = owned sum of (b - A x_t)^2 for t < h, reduced in a
  * fixed order.  No stop test and no residual tail: the caller (the slab
  * engine) decides per cycle.  Asynchronous.  Replaces, per slab, h iterations

@@ -760,7 +760,8 @@ int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
         out->launches = 1;
     } else if (op->sweeps_per_pass > 1 && op->tb3.supported) {
         CUDA_TRY(tb3_launch_cycle(op->tb3, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,
-                                  op->partials, op->hist, op->out_i, op->out_d, st));
+                                  op->partials, op->hist, op->out_i, op->out_d, st, 0, op->g.nz,
+                                  nullptr));
         out->launches = 1;
     } else if (op->p3.supported) {
         CUDA_TRY(launch3d_cycle(op->p3, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,
@@ -844,14 +845,20 @@ int srj_tb_pass(srj_op* op, double* x, double* x_alt, const double* b,
                 double* sums_dev, void* stream) {
     if (!op || !x || !x_alt || !b || !omegas_dev || !sums_dev)
         return fail(SRJ_BAD_ARGUMENT, "null argument");
-    if (!(op->tb.supported || op->tbv.supported))
+    if (!(op->tb.supported || op->tbv.supported || op->tb3.supported))
         return fail(SRJ_BAD_ARGUMENT, "no temporally blocked kernel for this operator");
-    if (h < 1 || h > kTbPassMax) return fail(SRJ_BAD_ARGUMENT, "sweeps per pass out of range");
-    if (row_lo < 0 || row_lo >= row_hi || row_hi > op->g.ny)
+    const bool is3d = op->tb3.supported;
+    if (h < 1 || h > (is3d ? op->tb3.sweeps : kTbPassMax))
+        return fail(SRJ_BAD_ARGUMENT, "sweeps per pass out of range");
+    if (row_lo < 0 || row_lo >= row_hi || row_hi > (is3d ? op->g.nz : op->g.ny))
         return fail(SRJ_BAD_ARGUMENT, "owned rows out of range");
     DeviceGuard guard(op->device);
     cudaStream_t st = (cudaStream_t)stream;
-    if (op->tbv.supported)
+    if (is3d)
+        CUDA_TRY(tb3_launch_cycle(op->tb3, op->g, x, x_alt, b, omegas_dev, h, -1.0, 1.0,
+                                  op->partials, op->hist, op->out_i, op->out_d, st, (int)row_lo,
+                                  (int)row_hi, sums_dev));
+    else if (op->tbv.supported)
         CUDA_TRY(tbv_launch_cycle(op->tbv, op->g, x, x_alt, b, omegas_dev, h, h, -1.0, 1.0,
                                   op->partials, op->hist, op->out_i, op->out_d, st, (int)row_lo,
                                   (int)row_hi, sums_dev));

@@ -46,16 +46,20 @@ struct Tb3Plan {
     int blocks = 0, tiles_x = 0, ntiles = 0;
     int sweeps = 0;
     int zc = 0, items = 0;  // planes per work item, work items (tiles x z-runs)
+    int num_sms = 0;
 };
 
 cudaError_t tb3_plan_init(Tb3Plan& plan, const Geom& g, int num_sms);
 
 // One cycle of M sweeps, plan.sweeps per pass; outputs as tb_launch_cycle.
-// x, x_alt and b must have zero ghost planes (Dirichlet).
+// The ghost planes of x and x_alt are the Dirichlet (zero) planes.
+// z_lo/z_hi: owned planes (slab with deep ghost planes; default the whole
+// grid); sums != nullptr: pass mode (one pass of M <= 2 sweeps, raw owned
+// sums of r^2 per sweep, no stop test, no residual tail).
 cudaError_t tb3_launch_cycle(const Tb3Plan& plan, const Geom& g, double* x, double* x_alt,
                              const double* b, const double* omegas, int M, double tol,
                              double baseline, double* partials, double* hist, int* out_i,
-                             double* out_d, cudaStream_t st);
+                             double* out_d, cudaStream_t st, int z_lo, int z_hi, double* sums);
 
 // 2D variable-coefficient temporal blocking (srj_tbvar.cu), up to 6 sweeps per pass.
 struct TbvPlan {

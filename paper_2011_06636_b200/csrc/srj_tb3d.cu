@@ -82,8 +82,10 @@ struct Tb3Ring {
     __device__ static __forceinline__ uint64_t* empty(int s) { return bars() + tb3d::D + s; }
 };
 
+// Work items: tiles x z-runs of zc planes over the owned planes [zlo, zhi)
+// (the whole grid, or a slab's owned planes between its deep ghost planes).
 struct Tb3Items {
-    int tiles_x, ntiles, zc, items;
+    int tiles_x, ntiles, zc, items, zlo, zhi;
 };
 
 __device__ __forceinline__ void fma_sq_if(double& acc, double r, bool cond) {
@@ -114,7 +116,7 @@ __device__ __forceinline__ void tb3_cursor_at(Tb3Cursor& c, const Tb3Items& it, 
         const int tile = item % it.ntiles, zci = item / it.ntiles;
         c.ox = (tile % it.tiles_x) * tb3d::TX;
         c.oy = (tile / it.tiles_x) * tb3d::TY;
-        const int z0 = zci * it.zc, z1 = min(z0 + it.zc, nz);
+        const int z0 = it.zlo + zci * it.zc, z1 = min(z0 + it.zc, it.zhi);
         c.z = z0 - 2;
         c.zend = z0 - 2 + tb3_steps(z0, z1) - 1;
     }
@@ -361,7 +363,7 @@ __device__ __forceinline__ void tb3_consume(const TbArgs& a, const Tb3Items& it,
     for (int item = blockIdx.x; item < it.items; item += gridDim.x) {
         const int tile = item % it.ntiles, zci = item / it.ntiles;
         const int ox = (tile % it.tiles_x) * TX, oy = (tile / it.tiles_x) * TY;
-        const int z0 = zci * it.zc, z1 = min(z0 + it.zc, nz);
+        const int z0 = it.zlo + zci * it.zc, z1 = min(z0 + it.zc, it.zhi);
         const int gx0 = ox - S + t.c0;  // grid column of this lane's first point
         t.rowg = t.rowacc = 0u;
 #pragma unroll
@@ -422,6 +424,7 @@ __device__ __forceinline__ void tb3_consume(const TbArgs& a, const Tb3Items& it,
     }
 }
 
+template <bool SLAB>
 __global__ void __launch_bounds__(tb3d::THREADS, 1)
     k_tb3d_cycle(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant__ CUtensorMap tm_x1,
                  const __grid_constant__ CUtensorMap tm_b, TbArgs a, Tb3Items it) {
@@ -439,7 +442,7 @@ __global__ void __launch_bounds__(tb3d::THREADS, 1)
     __syncthreads();
     uint32_t ld = 0;
     const CUtensorMap* const tmx[2] = {&tm_x0, &tm_x1};
-    tb_run_cycle<S, F3D, false, true>(
+    tb_run_cycle<S, F3D, SLAB, !SLAB>(
         a, (int)blockIdx.x < it.items,
         [&](int in, double* xout, int k0, int h, double (&acc)[S], bool accumulate, bool) {
             if (h == 0)  // residual of the cycle's final iterate
@@ -472,18 +475,24 @@ static int tb3_choose_zc(int ntiles, int slots, int nz) {
     return std::max(1, std::min(best_zc, nz));
 }
 
+template <bool SLAB>
+static cudaError_t tb3_attr() {
+    return cudaFuncSetAttribute(k_tb3d_cycle<SLAB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)tb3d::SMEM);
+}
+
 cudaError_t tb3_plan_init(Tb3Plan& plan, const Geom& g, int num_sms) {
     plan = Tb3Plan();
     // TMA needs a 16-byte row pitch (even nx).
     if (g.fam != F3D || (g.nx & 1) || !tma_available()) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(k_tb3d_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)tb3d::SMEM);
-    if (e != cudaSuccess) return e;
+    cudaError_t e;
+    if ((e = tb3_attr<false>()) != cudaSuccess || (e = tb3_attr<true>()) != cudaSuccess) return e;
     int per_sm = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tb3d_cycle, tb3d::THREADS,
-                                                           tb3d::SMEM)) != cudaSuccess)
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tb3d_cycle<false>,
+                                                           tb3d::THREADS, tb3d::SMEM)) != cudaSuccess)
         return e;
     if (per_sm < 1) return cudaSuccess;
+    plan.num_sms = num_sms;
     plan.tiles_x = (g.nx + tb3d::TX - 1) / tb3d::TX;
     plan.ntiles = plan.tiles_x * ((g.ny + tb3d::TY - 1) / tb3d::TY);
     plan.zc = tb3_choose_zc(plan.ntiles, num_sms, g.nz);
@@ -498,7 +507,7 @@ cudaError_t tb3_plan_init(Tb3Plan& plan, const Geom& g, int num_sms) {
 cudaError_t tb3_launch_cycle(const Tb3Plan& plan, const Geom& g, double* x, double* x_alt,
                              const double* b, const double* omegas, int M, double tol,
                              double baseline, double* partials, double* hist, int* out_i,
-                             double* out_d, cudaStream_t st) {
+                             double* out_d, cudaStream_t st, int z_lo, int z_hi, double* sums) {
     if ((((uintptr_t)x | (uintptr_t)x_alt | (uintptr_t)b) & 15) != 0)
         return cudaErrorMisalignedAddress;
     const long long plane = (long long)g.nx * g.ny;
@@ -527,17 +536,26 @@ cudaError_t tb3_launch_cycle(const Tb3Plan& plan, const Geom& g, double* x, doub
     a.out_d = out_d;
     a.tiles_x = plan.tiles_x;
     a.ntiles = plan.ntiles;
-    a.row_lo = 0;
-    a.row_hi = g.ny;
-    a.sums = nullptr;
+    a.row_lo = z_lo;
+    a.row_hi = z_hi;
+    a.sums = sums;
     Tb3Items it;
     it.tiles_x = plan.tiles_x;
     it.ntiles = plan.ntiles;
-    it.zc = plan.zc;
-    it.items = plan.items;
+    it.zlo = z_lo;
+    it.zhi = z_hi;
+    if (z_lo == 0 && z_hi == g.nz) {
+        it.zc = plan.zc;
+        it.items = plan.items;
+    } else {
+        const int nzr = z_hi - z_lo;
+        it.zc = tb3_choose_zc(plan.ntiles, plan.num_sms, nzr);
+        it.items = plan.ntiles * ((nzr + it.zc - 1) / it.zc);
+    }
+    const int blocks = std::max(1, std::min(plan.num_sms, it.items));
     void* args[] = {&m0, &m1, &mb, &a, &it};
-    return cudaLaunchCooperativeKernel((const void*)k_tb3d_cycle, dim3(plan.blocks),
-                                       dim3(tb3d::THREADS), args, tb3d::SMEM, st);
+    const void* fn = sums ? (const void*)k_tb3d_cycle<true> : (const void*)k_tb3d_cycle<false>;
+    return cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(tb3d::THREADS), args, tb3d::SMEM, st);
 }
 
 }  // namespace srj

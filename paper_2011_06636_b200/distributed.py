@@ -439,25 +439,33 @@ def local_slabs(family: str, shape, world: int, ranks, device, face_x=None, face
 # Temporally blocked row slabs (2D): deep ghost rows, one exchange per pass
 # ---------------------------------------------------------------------------
 
-TB_GHOST = 6  # ghost rows per interior side = sweeps per pass (srj_tb_pass)
+TB_GHOST = 6   # 2D: ghost rows per interior side = sweeps per pass (srj_tb_pass)
+TB3_GHOST = 2  # 3D: ghost planes per interior side = sweeps per pass
+
+
+def tb_ghost(family: str) -> int:
+    """Deep-halo width (= most sweeps one srj_tb_pass fuses) of a family."""
+    return TB3_GHOST if family == "3d7" else TB_GHOST
 
 
 class TbSlab:
-    """A 2D row slab extended by TB_GHOST ghost rows toward each neighbour (none
-    on a Dirichlet face).  Its operator covers the extended rows -- faces, b
-    and the iterate of the ghost rows included -- so one srj_tb_pass of up to
-    TB_GHOST sweeps updates the ghost rows as ring points and stores the owned
-    rows exactly as the single-GPU solve would."""
+    """A 2D row slab (3D z slab) extended by `ghost` ghost rows (planes) toward
+    each neighbour (none on a Dirichlet face): TB_GHOST = 6 rows in 2D,
+    TB3_GHOST = 2 planes in 3D.  Its operator covers the extended rows -- faces,
+    b and the iterate of the ghost rows included -- so one srj_tb_pass of up to
+    `ghost` sweeps updates the ghost rows as ring points and stores the owned
+    rows exactly as the single-GPU solve would.  A "row" is one x-row in 2D and
+    one xy plane in 3D (`unit` points)."""
 
     def __init__(self, layout: SlabLayout, rank: int, device, dx2: float | None = None,
                  face_x=None, face_y=None):
-        if layout.family not in ("2d5", "2d5var"):
-            raise ValueError("temporally blocked slabs are 2D row slabs")
+        if layout.family not in ("2d5", "2d5var", "3d7"):
+            raise ValueError("temporally blocked slabs are 2D row slabs or 3D z slabs")
         self.layout = layout
         self.rank = rank
         self.start, self.count = layout.span(rank)
         nx = layout.shape[0]
-        g = TB_GHOST
+        g = self.ghost = tb_ghost(layout.family)
         self.g_lo = g if rank > 0 else 0
         self.g_hi = g if rank < layout.world - 1 else 0
         rows = self.count + self.g_lo + self.g_hi
@@ -469,11 +477,13 @@ class TbSlab:
         else:
             if dx2 is None:
                 dx2 = (nx + 1.0) ** 2
-            self.A = StencilOperator("2d5", (nx, rows), dx2=dx2, device=device)
+            shape = (nx, rows) if layout.family == "2d5" else (nx, layout.shape[1], rows)
+            self.A = StencilOperator(layout.family, shape, dx2=dx2, device=device)
         if not self.A.describe()["tb_supported"]:
             raise ValueError("no temporally blocked kernel for this grid (odd nx?)")
         self.device = device
-        self.nx = nx
+        self.unit = layout.plane_points  # points per row (2D) / plane (3D)
+        self.nx = self.unit
         self.row0 = r0
         self.x = self.A.new_field()
         self.x_alt = self.A.new_field()
@@ -483,16 +493,16 @@ class TbSlab:
     @property
     def offset(self) -> int:
         """Global flat index of the slab's first OWNED point."""
-        return self.start * self.nx
+        return self.start * self.unit
 
     @property
     def owned(self) -> tuple[int, int]:
         return self.g_lo, self.g_lo + self.count
 
     def rows(self, field: Field, r0: int, r1: int):
-        """View of extended rows [r0, r1) of a Field."""
+        """View of extended rows (planes) [r0, r1) of a Field."""
         h = field.halo
-        return field.buf[h + r0 * self.nx:h + r1 * self.nx]
+        return field.buf[h + r0 * self.unit:h + r1 * self.unit]
 
     def interior(self, field: Field):
         lo, hi = self.owned
@@ -506,7 +516,7 @@ class LocalTbExchanger(LocalExchanger):
     """Virtual ranks in one process: deep ghost rows by device copies."""
 
     def start_rows(self, slabs, fields):
-        g = TB_GHOST
+        g = slabs[0].ghost
         for lo, hi, flo, fhi in zip(slabs[:-1], slabs[1:], fields[:-1], fields[1:]):
             a, b = lo.owned
             c, d = hi.owned
@@ -521,7 +531,7 @@ class TorchTbExchanger(TorchExchanger):
     def start_rows(self, slabs, fields):
         (s,), (f,) = slabs, fields
         dist = self.dist
-        g = TB_GHOST
+        g = s.ghost
         a, b = s.owned
         ops = []
         if self.rank > 0:
@@ -534,15 +544,17 @@ class TorchTbExchanger(TorchExchanger):
 
 
 class TbSlabSolver(SlabSolver):
-    """`solve` over temporally blocked row slabs: per cycle, passes of up to
-    TB_GHOST sweeps, each one deep ghost-row exchange plus one srj_tb_pass;
+    """`solve` over temporally blocked slabs: per cycle, passes of up to
+    `ghost` sweeps, each one deep ghost-row exchange plus one srj_tb_pass;
     the residual of x_M over the owned rows; one all-gather of the per-sweep
     owned sums; the same stop / rollback protocol as SlabSolver."""
 
     def __init__(self, slabs: list[TbSlab], exchanger):
         super().__init__(slabs, exchanger, engine=None)
-        if any(s.count < TB_GHOST for s in slabs):
-            raise ValueError(f"every slab needs at least {TB_GHOST} rows")
+        g = slabs[0].ghost
+        if any(s.count < g for s in slabs):
+            raise ValueError(f"every slab needs at least {g} rows")
+        self.ghost = g
         self._omega_cache = {}
 
     # -- data ---------------------------------------------------------------
@@ -551,7 +563,7 @@ class TbSlabSolver(SlabSolver):
         neighbours' b, which never changes)."""
         for s in self.slabs:
             n_ext = s.A.n
-            lo = s.row0 * s.nx
+            lo = s.row0 * s.unit
             if b is not None:
                 s.b.copy_(np.asarray(b)[lo:lo + n_ext])
             elif seed is not None:
@@ -568,7 +580,7 @@ class TbSlabSolver(SlabSolver):
         base, extra = divmod(self.layout.planes, self.layout.world)
         size = (base + (1 if extra else 0)) * self.layout.plane_points
         out = torch.zeros(size, dtype=torch.float64, device=s.x.buf.device)
-        out[:s.count * s.nx].copy_(s.interior(s.x))
+        out[:s.count * s.unit].copy_(s.interior(s.x))
         return out
 
     # -- kernels over all local slabs ----------------------------------------
@@ -585,10 +597,10 @@ class TbSlabSolver(SlabSolver):
         return t
 
     def _passes(self, om, sums, k_end: int) -> None:
-        """Sweeps 0 .. k_end-1 of the cycle in passes of <= TB_GHOST."""
+        """Sweeps 0 .. k_end-1 of the cycle in passes of <= ghost."""
         k = 0
         while k < k_end:
-            h = min(TB_GHOST, k_end - k)
+            h = min(self.ghost, k_end - k)
             self._exchange_rows()
             for s, sm in zip(self.slabs, sums):
                 lo, hi = s.owned
@@ -666,5 +678,6 @@ def local_tb_slabs(family: str, shape, world: int, ranks, device, face_x=None, f
 
 
 __all__ = ["SlabLayout", "Slab", "LocalExchanger", "TorchExchanger", "DeviceEngine",
-           "SlabSolver", "local_slabs", "PARTS", "ABSOLUTE_L2", "TB_GHOST", "TbSlab",
+           "SlabSolver", "local_slabs", "PARTS", "ABSOLUTE_L2", "TB_GHOST", "TB3_GHOST",
+           "tb_ghost", "TbSlab",
            "LocalTbExchanger", "TorchTbExchanger", "TbSlabSolver", "local_tb_slabs"]

@@ -173,9 +173,10 @@ class DeviceOperator:
 
     def tb_pass(self, x: Field, x_alt: Field, b: Field, omegas_ptr: int, h: int, row_lo: int,
                 row_hi: int, sums_ptr: int) -> None:
-        """One temporally blocked pass (h <= 6 sweeps) storing only the owned rows
-        [row_lo, row_hi) into x_alt; owned sums of r^2 per sweep at `sums_ptr`
-        (device).  Rows outside are a slab's deep ghost rows (srj_tb_pass)."""
+        """One temporally blocked pass (h <= 6 sweeps in 2D, <= 2 in 3D) storing
+        only the owned rows (3D: planes) [row_lo, row_hi) into x_alt; owned sums
+        of r^2 per sweep at `sums_ptr` (device).  Rows outside are a slab's deep
+        ghost rows (srj_tb_pass)."""
         _lib.check(_lib.lib().srj_tb_pass(
             self.handle, x.ptr, x_alt.ptr, b.ptr, ctypes.c_void_p(omegas_ptr), int(h),
             int(row_lo), int(row_hi), ctypes.c_void_p(sums_ptr), _stream_handle(self.device)),

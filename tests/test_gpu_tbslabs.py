@@ -1,7 +1,8 @@
-"""Temporally blocked 2D row slabs (srj_tb_pass + deep ghost rows) on the GPU.
+"""Temporally blocked slabs (srj_tb_pass + deep ghost rows / planes) on the GPU.
 
 Several extended slabs of one grid live on cuda:0 (virtual ranks) and exchange
-their TB_GHOST-deep ghost rows by device copies before each pass.  Iterates
+their deep ghost rows (2D: TB_GHOST = 6 rows, 3D: TB3_GHOST = 2 planes) by
+device copies before each pass.  Iterates
 must be bit-identical to the reference for every slab count, the scheme
 sequence identical; the pass kernel alone is checked against the oracle.
 """
@@ -18,6 +19,7 @@ import _parity as P
 pytestmark = pytest.mark.gpu
 
 CASES = ["c2_64", "c2_37", "c4_32", "c4_64", "budget_midcycle_2d"]
+CASES_3D = ["c3_16", "c3_32", "c3_48", "poisson3d_24_ones", "fixed2362_3d"]
 
 
 def _rows(rep):
@@ -90,3 +92,65 @@ def test_tb_pass_owned_rows_vs_oracle(family):
         assert np.all(got[:lo] == 123.0) and np.all(got[hi:] == 123.0), h
         np.testing.assert_allclose(sums.cpu().numpy(), sq, rtol=1e-12)
         assert all(math.isfinite(v) for v in sq)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+@pytest.mark.parametrize("name", CASES_3D)
+def test_tb_z_slabs_match_reference(name, world):
+    import torch
+
+    import paper_2011_06636_b200 as srj
+    from paper_2011_06636_b200.distributed import (LocalTbExchanger, TbSlabSolver,
+                                                   local_tb_slabs)
+    c = P.case(name)
+    fam, n, b, _, _ = P.case_inputs(c)
+    assert fam == "3d7"
+    if n % 2:
+        pytest.skip("temporal blocking needs an even row length")
+    if n // world < 2:
+        pytest.skip("slabs need at least TB3_GHOST planes")
+    slabs = local_tb_slabs(fam, (n, n, n), world, range(world), torch.device("cuda", 0))
+    assert all(s.A.describe()["cycle_kernel"] == 5 for s in slabs)
+    solver = TbSlabSolver(slabs, LocalTbExchanger(world))
+    solver.load(b=b)
+    rule = srj.StoppingRule(c["norm"], c["tol"], c.get("max_iterations", 10**9))
+    ctrl = c["controller"]
+    controller = srj.FixedM(int(ctrl.split(":")[1])) if ctrl.startswith("fixed:") else srj.Heuristic()
+    rep = solver.solve(controller, rule, record_history=False)
+    P.assert_trace_matches(c, _rows(rep), rep.total_iterations, rep.converged, x=solver.gather())
+
+
+@pytest.mark.parametrize("dims,lo,hi", [((130, 40, 14), 2, 12), ((64, 70, 9), 0, 7),
+                                        ((62, 33, 6), 2, 6)])
+def test_tb3_pass_owned_planes_vs_oracle(dims, lo, hi):
+    """One 3D srj_tb_pass of h <= 2 sweeps over owned planes [lo, hi): owned
+    planes equal the oracle's sweeps, planes outside are never written, the
+    per-sweep sums are the owned r^2."""
+    import torch
+
+    import paper_2011_06636_b200 as srj
+    from oracle import srj_oracle as O
+    nx, ny, nz = dims
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(nx + ny + nz)
+    A = srj.StencilOperator("3d7", dims, dx2=5.0, device=dev)
+    op = O.StencilCPU("3d7", nx, ny, nz, 5.0)
+    b = rng.uniform(-1, 1, A.n)
+    x0 = rng.uniform(-1, 1, A.n)
+    pl = nx * ny
+    for h in (1, 2):
+        omegas = rng.uniform(0.4, 2.6, h)
+        xs, sq = [x0], []
+        for w in omegas:
+            r, _ = op.residual(xs[-1], b)
+            sq.append(float(np.sum(r[lo * pl:hi * pl] ** 2)))
+            xs.append(op.update(xs[-1], r, w))
+        x = A.field(x0)
+        x_alt = A.field(np.full(A.n, 123.0))
+        om = torch.tensor(omegas, dtype=torch.float64, device=dev)
+        sums = torch.zeros(h, dtype=torch.float64, device=dev)
+        A.tb_pass(x, x_alt, A.field(b), om.data_ptr(), h, lo, hi, sums.data_ptr())
+        got = x_alt.interior.cpu().numpy()
+        assert np.array_equal(got[lo * pl:hi * pl], xs[h][lo * pl:hi * pl]), h
+        assert np.all(got[:lo * pl] == 123.0) and np.all(got[hi * pl:] == 123.0), h
+        np.testing.assert_allclose(sums.cpu().numpy(), sq, rtol=1e-12)

@@ -33,6 +33,7 @@ class FakeTbSlab:
     def __init__(self, layout, rank):
         self.layout = layout
         self.start, self.count = layout.span(rank)
+        self.ghost = TB_GHOST
         self.g_lo = TB_GHOST if rank > 0 else 0
         self.g_hi = TB_GHOST if rank < layout.world - 1 else 0
         self.nx = NX
