@@ -17,12 +17,15 @@
 // with c_w = fx[y][x], c_e = fx[y][x+1], c_s = fy[y][x], c_n = fy[y+1][x].
 // A face product belongs to one point pair, so (unlike the constant case) x
 // itself is exchanged: west/east by warp shuffle, north/south through the warp
-// edge rows.  Per point the thread keeps x, b, c_w, c_s and inv in registers
+// edge rows.  Per point the thread keeps x, b, c_w, c_s and diag in registers
 // (loaded once per tile); c_e is the east point's c_w (own register or one
 // shuffle per row per tile), c_n the south face of the row below (own register
 // or the next warp's first row, published once per tile).  inv is precomputed
 // once per operator (tbv_plan_init) with the reference's division, so it stays
-// bit-identical; diag is recomputed per sub-sweep (3 DADD, no extra registers).
+// bit-identical; per tile each thread copies its inv values into a private
+// shared-memory slot (the stage is refilled by the next tile's copy) and keeps
+// diag in registers, computed once per tile (3 DADD per point per tile instead
+// of per sub-sweep).
 //
 // Staged per tile: x, b, c_w (over the 16-byte-pitch copy of fx), c_s (fy) and
 // inv boxes, all RX x RY at the region origin; zero fill outside the grid.
@@ -51,7 +54,7 @@ struct Cfg {
     static constexpr int HBUF = 2 * HROWS * RX;    // top + bottom rows, one parity
     static constexpr int CSE = HROWS * RX;         // first-row c_s of every warp
     static constexpr size_t SMEM =
-        (size_t)(NST * STAGE + 2 * HBUF + CSE) * sizeof(double) + 32;
+        (size_t)(NST * STAGE + 2 * HBUF + CSE + STAGE) * sizeof(double) + 32;
     static constexpr uint32_t TX_BYTES = NST * STAGE * sizeof(double);
 };
 
@@ -68,7 +71,8 @@ extern __shared__ __align__(128) double tbv_smem[];
 
 struct TbvLayout {
     using C = tbv::Cfg;
-    static constexpr int ST = 0, H = C::NST * C::STAGE, CSE = H + 2 * C::HBUF, BAR = CSE + C::CSE;
+    static constexpr int ST = 0, H = C::NST * C::STAGE, CSE = H + 2 * C::HBUF, INV = CSE + C::CSE,
+                         BAR = INV + C::STAGE;
     // stages: 0 x, 1 b, 2 c_w, 3 c_s, 4 inv
     __device__ static __forceinline__ double* st(int k) { return tbv_smem + ST + k * C::STAGE; }
     __device__ static __forceinline__ double* top(int t) { return tbv_smem + H + (t & 1) * C::HBUF; }
@@ -76,6 +80,8 @@ struct TbvLayout {
         return tbv_smem + H + (t & 1) * C::HBUF + C::HROWS * C::RX;
     }
     __device__ static __forceinline__ double* cse() { return tbv_smem + CSE; }
+    // the tile's 1/diag, copied out of the stage (thread-private positions)
+    __device__ static __forceinline__ double* inv() { return tbv_smem + INV; }
     __device__ static __forceinline__ uint64_t* bar() {
         return reinterpret_cast<uint64_t*>(tbv_smem + BAR);
     }
@@ -118,7 +124,7 @@ __device__ __forceinline__ void tbv_issue(const TbvArgs& a, const CUtensorMap* t
 struct TbvRegs {
     using C = tbv::Cfg;
     double x[C::V][C::CW], b[C::V][C::CW];
-    double cw[C::V][C::CW], cs[C::V][C::CW], inv[C::V][C::CW];
+    double cw[C::V][C::CW], cs[C::V][C::CW], dg[C::V][C::CW];  // dg: diagonal
     double ce[C::V];   // east face of column CW-1 (= next lane's c_w of column 0)
     double cn[C::CW];  // north face of row V-1 (= next warp's c_s of row 0)
 };
@@ -147,6 +153,8 @@ __device__ __forceinline__ void tbv_sweeps(TbvRegs& R, const double* omegas, int
         auto row = [&](int v, const double (&xs)[CW], const double (&xn)[CW]) {
             const double xw = __shfl_up_sync(0xffffffffu, R.x[v][CW - 1], 1);
             const double xe = __shfl_down_sync(0xffffffffu, R.x[v][0], 1);
+            double iv[CW];
+            ld2(iv, L::inv() + (warp * V + v) * RX + col);
             double xo[CW];
 #pragma unroll
             for (int j = 0; j < CW; ++j) {
@@ -154,7 +162,7 @@ __device__ __forceinline__ void tbv_sweeps(TbvRegs& R, const double* omegas, int
                 const double c_e = j == CW - 1 ? R.ce[v] : R.cw[v][j + 1];
                 const double c_s = R.cs[v][j];
                 const double c_n = v == V - 1 ? R.cn[j] : R.cs[v + 1][j];
-                const double diag = DADD(DADD(DADD(c_w, c_e), c_s), c_n);
+                const double diag = R.dg[v][j];
                 const double x_w = j == 0 ? xw : R.x[v][j - 1];
                 const double x_e = j == CW - 1 ? xe : R.x[v][j + 1];
                 double y = DMUL(-c_s, xs[j]);  // 0 + (-c_s) x_s (see header)
@@ -163,7 +171,7 @@ __device__ __forceinline__ void tbv_sweeps(TbvRegs& R, const double* omegas, int
                 y = DADD(y, DMUL(-c_e, x_e));
                 y = DADD(y, DMUL(-c_n, xn[j]));
                 const double rr = DSUB(R.b[v][j], y);
-                const double xnew = relax(R.x[v][j], R.inv[v][j], rr, w);
+                const double xnew = relax(R.x[v][j], iv[j], rr, w);
                 const int bit = v * CW + j;
                 if constexpr (!MASKED && kAligned)
                     sq[j] = fma(rr, rr, sq[j]);  // owned: decided per thread below
@@ -281,7 +289,9 @@ __device__ __forceinline__ void tbv_pass(const TbvArgs& a, const CUtensorMap* tm
             ld2(R.b[v], L::st(1) + o);
             ld2(R.cw[v], L::st(2) + o);
             ld2(R.cs[v], L::st(3) + o);
-            ld2(R.inv[v], L::st(4) + o);
+            double iv[CW];
+            ld2(iv, L::st(4) + o);
+            st2(L::inv() + o, iv);
         }
         st2(L::top(0) + (warp + 1) * RX + c0, R.x[0]);
         st2(L::bot(0) + (warp + 1) * RX + c0, R.x[V - 1]);
@@ -290,6 +300,15 @@ __device__ __forceinline__ void tbv_pass(const TbvArgs& a, const CUtensorMap* tm
         for (int v = 0; v < V; ++v) R.ce[v] = __shfl_down_sync(0xffffffffu, R.cw[v][0], 1);
         __syncthreads();  // stages consumed, edge rows published
         ld2(R.cn, L::cse() + (warp + 2) * RX + c0);
+        // diagonal once per tile (reference assembly order)
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+#pragma unroll
+            for (int j = 0; j < CW; ++j) {
+                const double c_e = j == CW - 1 ? R.ce[v] : R.cw[v][j + 1];
+                const double c_n = v == V - 1 ? R.cn[j] : R.cs[v + 1][j];
+                R.dg[v][j] = DADD(DADD(DADD(R.cw[v][j], c_e), R.cs[v][j]), c_n);
+            }
         if (threadIdx.x == 0 && q + (int)gridDim.x < a.ntiles)
             tbv_issue<SLAB>(a, tm_in, m, q + gridDim.x);
         if (masked)
