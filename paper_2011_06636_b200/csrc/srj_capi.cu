@@ -220,100 +220,181 @@ __global__ void __launch_bounds__(kSmall1dThreads) k_small_cycle_1d(CycleArgs a)
 // warp w holds P consecutive points [(32w + l) P, +P) -- x, b and p = c*x in
 // registers for the whole cycle.  Neighbours inside a lane are registers, across
 // lanes one shuffle each way, across warps the edge p of the neighbouring warps
-// through shared memory (double-buffered by sweep parity).  Per sweep: residual
-// r_k of x_k at every point, warp butterfly of r^2 into red[parity][warp],
-// x_{k+1} committed (x_k kept for a stop at k), edge p published, ONE
-// __syncthreads, then every warp reduces the 4 partials in warp order
-// (identical bits everywhere) and applies the stop test.  Points past n are
-// held at 0.  Same protocol and outputs as k_cycle.
+// through shared memory (double-buffered by sweep parity), one __syncthreads
+// per sweep.
+//
+// Batched stop test.  A sweep's only output besides x_{k+1} is the lane's
+// partial sum of r_k^2; sweeps run in batches of K = 16 with the partials kept
+// in registers, then one transposed warp butterfly reduces all K at once
+// (16 shuffles instead of 5 per sweep) and warp 0 applies the reference's
+// per-sweep stop test (solver.py:216-222, 235-239) to the K residuals in order.
+// A stop at sweep kb+s of the batch restores the batch's input x_kb (a register
+// snapshot) and replays s sweeps.  Iterates are bit-identical to the reference
+// (the diagonal term is fma(p, -2, y): c_diag = -2 c_off exactly, see srj_tb.cu
+// for the identity and the leading "0 +"), residual norms are summed in a
+// fixed order.  FULL: n == 256 P (no held points past n).
 constexpr int kReg1dWarps = 8;
+constexpr int kReg1dBatch = 16;
 
-template <int P>
+// The register kernel applies c_diag*x as -2*p (exact: c_diag = -2 c_off).
+static bool reg1d_ok(const Geom& g) {
+    return g.fam == F1D && g.nx <= 32 * kReg1dWarps * 16 && g.c_diag == -2.0 * g.c_off;
+}
+
+template <int P, bool FULL>
 __global__ void __launch_bounds__(32 * kReg1dWarps) k_reg_cycle_1d(CycleArgs a) {
-    __shared__ double edge[2][2][kReg1dWarps + 2];  // [parity][first|last][warp + 1]
-    __shared__ double red[2][kReg1dWarps];
+    constexpr int K = kReg1dBatch, NW = kReg1dWarps;
+    __shared__ double edge[2][2][NW + 2];  // [parity][first|last][warp + 1]
+    __shared__ double red[K][NW + 1];
+    __shared__ double stop_sum;
+    __shared__ int stop_at, stop_status;
     const int n = a.g.nx;
-    const double c = a.g.c_off, d = a.g.c_diag, inv = a.g.inv_diag;
+    const double c = a.g.c_off, inv = a.g.inv_diag;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int i0 = (wid * 32 + lane) * P;
-    double x[P], xo[P], b[P], p[P];
+    double x[P], b[P], p[P], xs[P];
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-        const bool in = i0 + j < n;
+        const bool in = FULL || i0 + j < n;
         x[j] = in ? a.xa[i0 + j] : 0.0;
         b[j] = in ? a.b[i0 + j] : 0.0;
         p[j] = DMUL(c, x[j]);
     }
     const double pz = DMUL(c, 0.0);  // ghost / past-n neighbour: c*0 (a no-op term)
-    if (threadIdx.x < 2 * 2 * (kReg1dWarps + 2)) (&edge[0][0][0])[threadIdx.x] = pz;
+    if (threadIdx.x < 2 * 2 * (NW + 2)) (&edge[0][0][0])[threadIdx.x] = pz;
     __syncthreads();
     if (lane == 0) edge[0][0][wid + 1] = p[0];
     if (lane == 31) edge[0][1][wid + 1] = p[P - 1];
     const double tb = a.tol * a.baseline;
     const double hi2 = a.tol > 0.0 ? DMUL(DMUL(tb, tb), 1.0 + 1e-12) : -1.0;
     __syncthreads();
-    int executed = a.M, status = kStatusRan, last = 0;
-    double S = 0.0;
-    bool have_old = false;
-    // omega of the next sweep is loaded one sweep ahead (its L2 latency would
-    // otherwise sit on every sweep's critical path)
-    double w_next = a.M > 0 ? __ldg(a.omegas) : 0.0;
-    for (int k = 0; k <= a.M; ++k) {
-        const bool tail = (k == a.M);
-        const int par = k & 1;
-        const double w = w_next;
-        if (k + 1 < a.M) w_next = __ldg(a.omegas + k + 1);
-        // neighbours across the lane / warp boundaries (old p)
+    int par = 0;
+    // One sweep: residual of the current x (returned as the lane's sum of r^2
+    // over its points), and x <- x + w inv r unless `update` is false.
+    auto sweep = [&](double w, bool update) -> double {
+        // branch-free: every lane reads the two edge words (broadcast) and the
+        // warp's end lanes select them
+        const double el = edge[par][1][wid];      // last point of warp-1
+        const double er = edge[par][0][wid + 2];  // first point of warp+1
         double pl = __shfl_up_sync(0xffffffffu, p[P - 1], 1);
         double pr = __shfl_down_sync(0xffffffffu, p[0], 1);
-        if (lane == 0) pl = edge[par][1][wid];       // last point of warp-1
-        if (lane == 31) pr = edge[par][0][wid + 2];  // first point of warp+1
+        pl = lane == 0 ? el : pl;
+        pr = lane == 31 ? er : pr;
         double r[P], acc = 0.0;
 #pragma unroll
         for (int j = 0; j < P; ++j) {
-            double y = DADD(0.0, j == 0 ? pl : p[j - 1]);
-            y = DADD(y, DMUL(d, x[j]));
+            double y = __fma_rn(p[j], -2.0, j == 0 ? pl : p[j - 1]);
             y = DADD(y, j == P - 1 ? pr : p[j + 1]);
             r[j] = DSUB(b[j], y);
-            if (i0 + j < n) acc = fma(r[j], r[j], acc);
+            if (FULL || i0 + j < n) acc = fma(r[j], r[j], acc);
         }
-        acc = warp_allsum(acc);
-        if (lane == 0) red[par][wid] = acc;
-        if (!tail) {
+        if (update) {
 #pragma unroll
             for (int j = 0; j < P; ++j) {
-                xo[j] = x[j];
-                x[j] = i0 + j < n ? relax(x[j], inv, r[j], w) : 0.0;
+                const double xn = relax(x[j], inv, r[j], w);
+                x[j] = (FULL || i0 + j < n) ? xn : 0.0;
                 p[j] = DMUL(c, x[j]);
             }
-            have_old = true;
             if (lane == 0) edge[par ^ 1][0][wid + 1] = p[0];
             if (lane == 31) edge[par ^ 1][1][wid + 1] = p[P - 1];
+            __syncthreads();
+            par ^= 1;
         }
-        __syncthreads();
-        S = red[par][0];
+        return acc;
+    };
+    const int M = a.M;
+    int executed = M, status = kStatusRan;
+    double S = 0.0;
+    for (int kb = 0;; kb = min(kb + K, M)) {
+        // sweeps kb .. kb+kk-1 (residual of x_k, then x_{k+1}); at kb == M the
+        // residual of x_M alone (the cycle's tail)
+        const bool tail = kb == M;
+        const int kk = tail ? 1 : min(K, M - kb);
 #pragma unroll
-        for (int q = 1; q < kReg1dWarps; ++q) S = DADD(S, red[par][q]);
-        if (k >= 1) {
-            last = k;
-            if (threadIdx.x == 0) a.hist[k] = S;  // converted below
-            if (!(S > hi2 && S < 1e300)) {
-                const double res = sqrt(S) / a.baseline;
-                if (!isfinite(res)) { executed = k; status = kStatusDiverged; break; }
-                if (res <= a.tol) { executed = k; status = kStatusConverged; break; }
+        for (int j = 0; j < P; ++j) xs[j] = x[j];
+        double v[K], wv[K];  // the batch's omegas, loaded up front (off the sweep chain)
+#pragma unroll
+        for (int s = 0; s < K; ++s) wv[s] = (!tail && s < kk) ? __ldg(a.omegas + kb + s) : 0.0;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            v[s] = 0.0;
+            if (s < kk) v[s] = sweep(wv[s], !tail);
+        }
+        // transposed butterfly: after the rounds lane l holds the warp sum of
+        // sweep (l >> 1) & (K-1) (fixed order; both lanes of a pair agree)
+#pragma unroll
+        for (int h = K / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
+            const bool hi = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < h; ++i) {
+                const double send = hi ? v[i] : v[i + h];
+                const double keep = hi ? v[i + h] : v[i];
+                v[i] = DADD(keep, __shfl_xor_sync(0xffffffffu, send, o));
             }
         }
+        v[0] = DADD(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
+        if ((lane & 1) == 0) red[(lane >> 1) & (K - 1)][wid] = v[0];
+        __syncthreads();
+        if (wid == 0) {
+            // lane s: the residual of x_{kb+s}, warp partials in warp order
+            double Ss = 0.0;
+            bool stop = false;
+            int st = kStatusRan;
+            if (lane < kk) {
+                Ss = red[lane][0];
+#pragma unroll
+                for (int q = 1; q < NW; ++q) Ss = DADD(Ss, red[lane][q]);
+                const int k = kb + lane;
+                if (k >= 1) {
+                    const double res = sqrt(Ss) / a.baseline;
+                    a.hist[k] = res;
+                    if (!(Ss > hi2 && Ss < 1e300)) {
+                        if (!isfinite(res)) { stop = true; st = kStatusDiverged; }
+                        else if (res <= a.tol) { stop = true; st = kStatusConverged; }
+                    }
+                }
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, stop);
+            const int first = m ? __ffs(m) - 1 : (tail ? 0 : -1);
+            if (first >= 0 && lane == first) {
+                stop_at = first;
+                stop_status = st;
+                stop_sum = Ss;
+            } else if (first < 0 && lane == kk - 1) {
+                stop_at = -1;
+                stop_sum = Ss;
+            }
+        }
+        __syncthreads();
+        const int s_stop = stop_at;
+        S = stop_sum;
+        if (s_stop >= 0) {
+            if (!tail) {
+                executed = kb + s_stop;
+                // x_{kb+s}: replay s sweeps from the batch's input
+#pragma unroll
+                for (int j = 0; j < P; ++j) {
+                    x[j] = xs[j];
+                    p[j] = DMUL(c, x[j]);
+                }
+                if (lane == 0) edge[par][0][wid + 1] = p[0];
+                if (lane == 31) edge[par][1][wid + 1] = p[P - 1];
+                __syncthreads();
+#pragma unroll
+                for (int s = 0; s < K; ++s)
+                    if (s < s_stop) sweep(wv[s], true);
+            }
+            status = stop_status;
+            break;
+        }
+        __syncthreads();  // stop_at / stop_sum are rewritten by the next batch
     }
-    // x_executed: the committed x, or x_k (kept in xo) after a stop at k < M
-    const bool use_old = executed < a.M && have_old;
     if (executed > 0) {
         double* dst = (executed & 1) ? a.xb : const_cast<double*>(a.xa);
 #pragma unroll
         for (int j = 0; j < P; ++j)
-            if (i0 + j < n) dst[i0 + j] = use_old ? xo[j] : x[j];
+            if (FULL || i0 + j < n) dst[i0 + j] = x[j];
     }
-    __syncthreads();  // thread 0's hist stores are visible to the CTA
-    for (int k = 1 + threadIdx.x; k <= last; k += blockDim.x) a.hist[k] = sqrt(a.hist[k]) / a.baseline;
     if (threadIdx.x == 0) {
         a.out_i[0] = executed;
         a.out_i[1] = status;
@@ -659,7 +740,7 @@ int srj_op_describe(const srj_op* op, srj_op_info* info) {
                             op->tb_kind == SRJ_TB_WARP_STREAM) ? SRJ_KERNEL_WS2D
                          : (op->sweeps_per_pass > 1 && op->tb.supported) ? SRJ_KERNEL_TB2D
                          : op->p2.supported                               ? SRJ_KERNEL_TILE2D
-                         : (op->g.fam == F1D && op->g.nx <= 32 * kReg1dWarps * 16) ? SRJ_KERNEL_REG1D
+                         : reg1d_ok(op->g) ? SRJ_KERNEL_REG1D
                          : (op->g.fam == F1D && op->g.nx <= kSmall1dMaxN) ? SRJ_KERNEL_SMALL1D
                                                                           : SRJ_KERNEL_GENERIC;
     return SRJ_OK;
@@ -689,13 +770,18 @@ static int launch_cycle(srj_op* op, const double* xa, double* xb, const double* 
     a.hist = op->hist;
     a.out_i = op->out_i;
     a.out_d = op->out_d;
-    if (!diff && op->g.fam == F1D && op->g.nx <= 32 * kReg1dWarps * 16) {
+    if (!diff && reg1d_ok(op->g)) {
         const int per = (op->g.nx + 32 * kReg1dWarps - 1) / (32 * kReg1dWarps);
+        const bool full = op->g.nx == per * 32 * kReg1dWarps;
         const dim3 grid(1), block(32 * kReg1dWarps);
-        if (per <= 2) k_reg_cycle_1d<2><<<grid, block, 0, st>>>(a);
-        else if (per <= 4) k_reg_cycle_1d<4><<<grid, block, 0, st>>>(a);
-        else if (per <= 8) k_reg_cycle_1d<8><<<grid, block, 0, st>>>(a);
-        else k_reg_cycle_1d<16><<<grid, block, 0, st>>>(a);
+#define SRJ_REG1D(PP)                                                          \
+    if (full) k_reg_cycle_1d<PP, true><<<grid, block, 0, st>>>(a);            \
+    else k_reg_cycle_1d<PP, false><<<grid, block, 0, st>>>(a)
+        if (per <= 2) { SRJ_REG1D(2); }
+        else if (per <= 4) { SRJ_REG1D(4); }
+        else if (per <= 8) { SRJ_REG1D(8); }
+        else { SRJ_REG1D(16); }
+#undef SRJ_REG1D
         CUDA_TRY(cudaGetLastError());
         return SRJ_OK;
     }
