@@ -66,6 +66,9 @@ def parse():
     ap.add_argument("--cycles", type=int, default=50, help="c5: heuristic cycles per step")
     ap.add_argument("--slabs", action="store_true",
                     help="c3/c4: use the slab solver even on one GPU (it is used for N > 1)")
+    ap.add_argument("--host-loop", action="store_true",
+                    help="run the controller loop on the host (one launch per cycle) even where "
+                         "the device-resident solve exists")
     ap.add_argument("--no-tb-slabs", action="store_true",
                     help="slabs: one sweep per launch instead of temporally blocked passes")
     return ap.parse_args()
@@ -413,7 +416,8 @@ def run_ours(args, rank, world, local):
 
     def one_solve():
         x.buf.zero_()
-        return solve_fields(A, b, x, x_alt, ctrl, rule, record_history=False)
+        return solve_fields(A, b, x, x_alt, ctrl, rule, record_history=False,
+                            device_loop=not args.host_loop)
 
     # warm-up (also builds every scheme the solve visits)
     rep = None
@@ -437,7 +441,24 @@ def run_ours(args, rank, world, local):
             launch_bytes.append(bpu * A.n * out.executed + RESIDUAL_BYTES[family] * A.n)
         return out
 
+    orig_solve_device = ops_mod.StencilOperator.solve_device
+    solve_launches = [0]
+
+    def timed_solve_device(self, *a, **kw):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out, recs = orig_solve_device(self, *a, **kw)
+        e1.record(stream)
+        e1.synchronize()
+        launch_ms.append(e0.elapsed_time(e1))
+        launch_bytes.append(sum(bpu * A.n * r.executed + RESIDUAL_BYTES[family] * A.n
+                                for r in recs if r.executed > 0))
+        solve_launches[0] += 1
+        return out, recs
+
     ops_mod.StencilOperator.run_cycle = timed_run_cycle
+    ops_mod.StencilOperator.solve_device = timed_solve_device
 
     step_ms = []
     sweeps = []
@@ -456,9 +477,12 @@ def run_ours(args, rank, world, local):
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
             sweeps.append(rep.total_iterations)
-            launches += len(rep.cycles) + 2  # cycle kernels + baseline/first residual
+            launches += 2  # baseline / first residual
         torch.cuda.synchronize()
+    # cycle kernels: one per cycle (host loop) or per srj_solve call (device loop)
+    launches += len(launch_ms)
     ops_mod.StencilOperator.run_cycle = orig_run_cycle
+    ops_mod.StencilOperator.solve_device = orig_solve_device
     if world > 1:
         dist.barrier()
     total_ms = sum(step_ms)

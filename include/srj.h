@@ -7,6 +7,7 @@
  * point below names the reference code it replaces:
  *
  *   srj_run_cycle      solver.run_cycle's sweep loop            solver.py:216-243
+ *   srj_solve          solver.solve's cycle loop on the device  solver.py:289-331
  *                      + the post-loop convergence test          solver.py:245-249
  *                      (x + w*(inv_diag*r), b - csr.dot(x), np.linalg.norm,
  *                       np.isfinite, per-sweep tol/budget tests, history)
@@ -173,6 +174,59 @@ int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
                   const double* omegas_dev, int32_t M, double tol, double baseline,
                   double res_before, int64_t budget, double* history_host,
                   srj_cycle_out* out, void* stream);
+
+/* Device-resident solve: the controller loop of solver.solve (solver.py:305-326)
+ * runs on the device between cycles, so a whole solve is one launch (or a few,
+ * see SRJ_SOLVE_PAUSED).  Cycle j applies the scheme of its level
+ * (omegas_all[level_off[l] .. level_off[l+1]), application order) with the
+ * srj_run_cycle semantics, starting from x (the final iterate ends in x or
+ * x_alt); between cycles the level moves as heuristic_next_level on the last
+ * finite residual ratio (mode 0, thresholds t_hi / t_lo), by +1 (mode 1,
+ * Increasing) or stays (mode 2, one fixed scheme).  The loop stops when a
+ * cycle converges (or the incoming residual is already <= tol), diverges, the
+ * sweep budget is spent, max_cycles records are written or the next cycle
+ * would pass hist_cap sweeps (paused: continue with next_level, res_next,
+ * prev_ratio and the result buffer).  recs_host receives one record per cycle
+ * (out->cycles entries), history_host (nullable) the relative residual after
+ * each sweep (out->sweeps entries).  Available where srj_op_solve_supported
+ * says so (the temporally blocked kernels).  Synchronises `stream`. */
+typedef struct srj_solve_args {
+    const double* omegas_all;  /* device */
+    const int32_t* level_off;  /* device, n_levels + 1 entries */
+    int32_t n_levels;
+    int32_t mode;              /* 0 heuristic, 1 increasing, 2 fixed */
+    int32_t level0;
+    int32_t max_cycles;
+    double t_hi, t_lo;
+    double res0;               /* residual entering the first cycle */
+    double prev_ratio0;        /* last finite residual ratio so far, NaN if none */
+    int64_t budget;            /* sweeps allowed: max_iterations - total so far */
+    int64_t hist_cap;          /* >= 10000; sweeps one call may record */
+} srj_solve_args;
+
+typedef struct srj_solve_rec {
+    int32_t level, M, executed, status;  /* status: enum srj_cycle_status */
+    double res_before, res_after;
+} srj_solve_rec;
+
+enum srj_solve_stop {
+    SRJ_SOLVE_PAUSED = 0, SRJ_SOLVE_CONVERGED = 1, SRJ_SOLVE_DIVERGED = 2, SRJ_SOLVE_BUDGET = 3
+};
+
+typedef struct srj_solve_out {
+    int32_t cycles;            /* records written */
+    int32_t stop;              /* enum srj_solve_stop */
+    int32_t result_in_alt;     /* 1: the last iterate is in x_alt */
+    int32_t next_level;        /* level of the next cycle (paused) */
+    double res_next;           /* residual entering the next cycle (paused) */
+    double prev_ratio;         /* last finite residual ratio (NaN if none) */
+    int64_t sweeps;            /* sweeps applied by this call */
+} srj_solve_out;
+
+int srj_op_solve_supported(const srj_op* op);
+int srj_solve(srj_op* op, double* x, double* x_alt, const double* b, const srj_solve_args* args,
+              double tol, double baseline, srj_solve_rec* recs_host, double* history_host,
+              srj_solve_out* out, void* stream);
 
 /* Same cycle under the solution-difference infinity norm (solver.py:200-203,
  * 224-228, 242-243): sweep k's norm is max|x_{k+1} - x_k| (bit-identical to

@@ -27,8 +27,10 @@ EXPORTED_SYMBOLS = (
     "srj_residual_sq",
     "srj_run_cycle", "srj_sweep", "srj_matvec", "srj_fill_uniform_rhs",
     "srj_op_planes", "srj_sweep_planes", "srj_run_cycle_diffinf", "srj_batch_cycles_1d",
-    "srj_op_set_temporal_kernel", "srj_tb_pass",
+    "srj_op_set_temporal_kernel", "srj_tb_pass", "srj_op_solve_supported", "srj_solve",
 )
+SOLVE_PAUSED, SOLVE_CONVERGED, SOLVE_DIVERGED, SOLVE_BUDGET = 0, 1, 2, 3
+SOLVE_HEURISTIC, SOLVE_INCREASING, SOLVE_FIXED = 0, 1, 2
 TB_TILE, TB_WARP_STREAM = 0, 1
 
 
@@ -53,6 +55,26 @@ class CycleOut(ctypes.Structure):
         ("executed", c_int32), ("status", c_int32), ("result_in_alt", c_int32),
         ("launches", c_int32), ("res_before", c_double), ("res_after", c_double),
     ]
+
+
+class SolveArgs(ctypes.Structure):
+    _fields_ = [
+        ("omegas_all", c_void_p), ("level_off", c_void_p),
+        ("n_levels", c_int32), ("mode", c_int32), ("level0", c_int32), ("max_cycles", c_int32),
+        ("t_hi", c_double), ("t_lo", c_double), ("res0", c_double), ("prev_ratio0", c_double),
+        ("budget", c_int64), ("hist_cap", c_int64),
+    ]
+
+
+class SolveRec(ctypes.Structure):
+    _fields_ = [("level", c_int32), ("M", c_int32), ("executed", c_int32), ("status", c_int32),
+                ("res_before", c_double), ("res_after", c_double)]
+
+
+class SolveOut(ctypes.Structure):
+    _fields_ = [("cycles", c_int32), ("stop", c_int32), ("result_in_alt", c_int32),
+                ("next_level", c_int32), ("res_next", c_double), ("prev_ratio", c_double),
+                ("sweeps", c_int64)]
 
 
 class OpInfo(ctypes.Structure):
@@ -108,6 +130,9 @@ def _declare(L):
                                    c_int64, c_void_p, c_int32, c_void_p]
     L.srj_tb_pass.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
                               c_int64, c_int64, c_void_p, c_void_p]
+    L.srj_op_solve_supported.argtypes = [c_void_p]
+    L.srj_solve.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, POINTER(SolveArgs), c_double,
+                            c_double, c_void_p, c_void_p, POINTER(SolveOut), c_void_p]
     for name in EXPORTED_SYMBOLS:
         if name not in ("srj_abi_version", "srj_last_error"):
             getattr(L, name).restype = c_int32

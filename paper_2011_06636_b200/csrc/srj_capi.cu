@@ -23,6 +23,7 @@
 
 #include "../../include/srj.h"
 #include "srj_common.cuh"
+#include "srj_tbdriver.cuh"
 #include "srj_stencil.cuh"
 #include "srj_2d.cuh"
 #include "srj_3d.cuh"
@@ -56,6 +57,7 @@ struct CycleArgs {
     int* out_i;            // executed, status
     double* out_d;         // final sum of squares, res_after
     int diff;              // 1: solution-difference infinity norm (no baseline, no lag)
+    SolveCtl ctl;          // device-resident solve (k_reg_cycle_1d<.., SOLVE>)
 };
 
 // Solution-difference norm cycle (reference solver.py:200-203,224-228,242-243):
@@ -241,7 +243,7 @@ static bool reg1d_ok(const Geom& g) {
     return g.fam == F1D && g.nx <= 32 * kReg1dWarps * 16 && g.c_diag == -2.0 * g.c_off;
 }
 
-template <int P, bool FULL>
+template <int P, bool FULL, bool SOLVE>
 __global__ void __launch_bounds__(32 * kReg1dWarps) k_reg_cycle_1d(CycleArgs a) {
     constexpr int K = kReg1dBatch, NW = kReg1dWarps;
     __shared__ double edge[2][2][NW + 2];  // [parity][first|last][warp + 1]
@@ -271,7 +273,7 @@ __global__ void __launch_bounds__(32 * kReg1dWarps) k_reg_cycle_1d(CycleArgs a) 
     int par = 0;
     // One sweep: residual of the current x (returned as the lane's sum of r^2
     // over its points), and x <- x + w inv r unless `update` is false.
-    auto sweep = [&](double w, bool update) -> double {
+    auto sweep = [&](double w, bool update) __attribute__((always_inline)) -> double {
         // branch-free: every lane reads the two edge words (broadcast) and the
         // warp's end lanes select them
         const double el = edge[par][1][wid];      // last point of warp-1
@@ -302,105 +304,174 @@ __global__ void __launch_bounds__(32 * kReg1dWarps) k_reg_cycle_1d(CycleArgs a) 
         }
         return acc;
     };
-    const int M = a.M;
-    int executed = M, status = kStatusRan;
-    double S = 0.0;
-    for (int kb = 0;; kb = min(kb + K, M)) {
-        // sweeps kb .. kb+kk-1 (residual of x_k, then x_{k+1}); at kb == M the
-        // residual of x_M alone (the cycle's tail)
-        const bool tail = kb == M;
-        const int kk = tail ? 1 : min(K, M - kb);
+    // One cycle of M sweeps with omegas[0..M): x (registers) ends as
+    // x_executed; hist[k] = relative residual of x_k (k = 1..); returns
+    // {executed, status} and the last residual's sum of squares in S.
+    auto cycle = [&](const int M, const double* __restrict__ omegas, double* __restrict__ hist,
+                     int& status, double& S) __attribute__((always_inline)) -> int {
+        int executed = M;
+        status = kStatusRan;
+        S = 0.0;
+        for (int kb = 0;; kb = min(kb + K, M)) {
+            // sweeps kb .. kb+kk-1 (residual of x_k, then x_{k+1}); at kb == M the
+            // residual of x_M alone (the cycle's tail)
+            const bool tail = kb == M;
+            const int kk = tail ? 1 : min(K, M - kb);
 #pragma unroll
-        for (int j = 0; j < P; ++j) xs[j] = x[j];
-        double v[K], wv[K];  // the batch's omegas, loaded up front (off the sweep chain)
+            for (int j = 0; j < P; ++j) xs[j] = x[j];
+            double v[K], wv[K];  // the batch's omegas, loaded up front (off the sweep chain)
 #pragma unroll
-        for (int s = 0; s < K; ++s) wv[s] = (!tail && s < kk) ? __ldg(a.omegas + kb + s) : 0.0;
+            for (int s = 0; s < K; ++s) wv[s] = (!tail && s < kk) ? __ldg(omegas + kb + s) : 0.0;
 #pragma unroll
-        for (int s = 0; s < K; ++s) {
-            v[s] = 0.0;
-            if (s < kk) v[s] = sweep(wv[s], !tail);
-        }
-        // transposed butterfly: after the rounds lane l holds the warp sum of
-        // sweep (l >> 1) & (K-1) (fixed order; both lanes of a pair agree)
-#pragma unroll
-        for (int h = K / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
-            const bool hi = (lane & o) != 0;
-#pragma unroll
-            for (int i = 0; i < h; ++i) {
-                const double send = hi ? v[i] : v[i + h];
-                const double keep = hi ? v[i + h] : v[i];
-                v[i] = DADD(keep, __shfl_xor_sync(0xffffffffu, send, o));
+            for (int s = 0; s < K; ++s) {
+                v[s] = 0.0;
+                if (s < kk) v[s] = sweep(wv[s], !tail);
             }
-        }
-        v[0] = DADD(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
-        if ((lane & 1) == 0) red[(lane >> 1) & (K - 1)][wid] = v[0];
-        __syncthreads();
-        if (wid == 0) {
-            // lane s: the residual of x_{kb+s}, warp partials in warp order
-            double Ss = 0.0;
-            bool stop = false;
-            int st = kStatusRan;
-            if (lane < kk) {
-                Ss = red[lane][0];
+            // transposed butterfly: after the rounds lane l holds the warp sum of
+            // sweep (l >> 1) & (K-1) (fixed order; both lanes of a pair agree)
 #pragma unroll
-                for (int q = 1; q < NW; ++q) Ss = DADD(Ss, red[lane][q]);
-                const int k = kb + lane;
-                if (k >= 1) {
-                    const double res = sqrt(Ss) / a.baseline;
-                    a.hist[k] = res;
-                    if (!(Ss > hi2 && Ss < 1e300)) {
-                        if (!isfinite(res)) { stop = true; st = kStatusDiverged; }
-                        else if (res <= a.tol) { stop = true; st = kStatusConverged; }
+            for (int h = K / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
+                const bool hi = (lane & o) != 0;
+#pragma unroll
+                for (int i = 0; i < h; ++i) {
+                    const double send = hi ? v[i] : v[i + h];
+                    const double keep = hi ? v[i + h] : v[i];
+                    v[i] = DADD(keep, __shfl_xor_sync(0xffffffffu, send, o));
+                }
+            }
+            v[0] = DADD(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
+            if ((lane & 1) == 0) red[(lane >> 1) & (K - 1)][wid] = v[0];
+            __syncthreads();
+            if (wid == 0) {
+                // lane s: the residual of x_{kb+s}, warp partials in warp order
+                double Ss = 0.0;
+                bool stop = false;
+                int st = kStatusRan;
+                if (lane < kk) {
+                    Ss = red[lane][0];
+#pragma unroll
+                    for (int q = 1; q < NW; ++q) Ss = DADD(Ss, red[lane][q]);
+                    const int k = kb + lane;
+                    if (k >= 1) {
+                        const double res = sqrt(Ss) / a.baseline;
+                        hist[k] = res;
+                        if (!(Ss > hi2 && Ss < 1e300)) {
+                            if (!isfinite(res)) { stop = true; st = kStatusDiverged; }
+                            else if (res <= a.tol) { stop = true; st = kStatusConverged; }
+                        }
                     }
                 }
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, stop);
-            const int first = m ? __ffs(m) - 1 : (tail ? 0 : -1);
-            if (first >= 0 && lane == first) {
-                stop_at = first;
-                stop_status = st;
-                stop_sum = Ss;
-            } else if (first < 0 && lane == kk - 1) {
-                stop_at = -1;
-                stop_sum = Ss;
-            }
-        }
-        __syncthreads();
-        const int s_stop = stop_at;
-        S = stop_sum;
-        if (s_stop >= 0) {
-            if (!tail) {
-                executed = kb + s_stop;
-                // x_{kb+s}: replay s sweeps from the batch's input
-#pragma unroll
-                for (int j = 0; j < P; ++j) {
-                    x[j] = xs[j];
-                    p[j] = DMUL(c, x[j]);
+                const unsigned m = __ballot_sync(0xffffffffu, stop);
+                const int first = m ? __ffs(m) - 1 : (tail ? 0 : -1);
+                if (first >= 0 && lane == first) {
+                    stop_at = first;
+                    stop_status = st;
+                    stop_sum = Ss;
+                } else if (first < 0 && lane == kk - 1) {
+                    stop_at = -1;
+                    stop_sum = Ss;
                 }
-                if (lane == 0) edge[par][0][wid + 1] = p[0];
-                if (lane == 31) edge[par][1][wid + 1] = p[P - 1];
-                __syncthreads();
-#pragma unroll
-                for (int s = 0; s < K; ++s)
-                    if (s < s_stop) sweep(wv[s], true);
             }
-            status = stop_status;
-            break;
+            __syncthreads();
+            const int s_stop = stop_at;
+            S = stop_sum;
+            if (s_stop >= 0) {
+                if (!tail) {
+                    executed = kb + s_stop;
+                    // x_{kb+s}: replay s sweeps from the batch's input
+#pragma unroll
+                    for (int j = 0; j < P; ++j) {
+                        x[j] = xs[j];
+                        p[j] = DMUL(c, x[j]);
+                    }
+                    if (lane == 0) edge[par][0][wid + 1] = p[0];
+                    if (lane == 31) edge[par][1][wid + 1] = p[P - 1];
+                    __syncthreads();
+#pragma unroll
+                    for (int s = 0; s < K; ++s)
+                        if (s < s_stop) sweep(wv[s], true);
+                }
+                status = stop_status;
+                __syncthreads();  // stop_* are rewritten by the next batch / cycle
+                return executed;
+            }
+            __syncthreads();  // stop_at / stop_sum are rewritten by the next batch
         }
-        __syncthreads();  // stop_at / stop_sum are rewritten by the next batch
-    }
-    if (executed > 0) {
-        double* dst = (executed & 1) ? a.xb : const_cast<double*>(a.xa);
+    };
+    if constexpr (!SOLVE) {
+        int status;
+        double S;
+        const int executed = cycle(a.M, a.omegas, a.hist, status, S);
+        if (executed > 0) {
+            double* dst = (executed & 1) ? a.xb : const_cast<double*>(a.xa);
+#pragma unroll
+            for (int j = 0; j < P; ++j)
+                if (FULL || i0 + j < n) dst[i0 + j] = x[j];
+        }
+        if (threadIdx.x == 0) {
+            a.out_i[0] = executed;
+            a.out_i[1] = status;
+            a.out_i[2] = executed & 1;
+            a.out_d[0] = S;
+            a.out_d[1] = sqrt(S) / a.baseline;
+        }
+    } else {
+        // Device-resident solve (srj_tbdriver.cuh tb_run_solve, same decisions):
+        // every thread runs the controller on identical values; x stays in
+        // registers across cycles and ends in xa.
+        const SolveCtl& cs = a.ctl;
+        int level = cs.level0, stop = kSolvePaused, cyc = 0;
+        long long total = 0;
+        double res_before = cs.res0, prev = cs.prev_ratio0;
+        for (; cyc < cs.max_cycles; ++cyc) {
+            const int off = cs.level_off[level];
+            const int Mfull = cs.level_off[level + 1] - off;
+            if (res_before <= a.tol) {  // solver.py:217-222, checked on the known residual
+                if (threadIdx.x == 0)
+                    cs.recs[cyc] = SolveRec{level, Mfull, 0, kStatusConverged, res_before, res_before};
+                stop = kSolveConverged;
+                ++cyc;
+                break;
+            }
+            const int Meff = (int)min((long long)Mfull, max(cs.budget - total, 0ll));
+            if (Meff == 0) {
+                if (threadIdx.x == 0)
+                    cs.recs[cyc] = SolveRec{level, Mfull, 0, kStatusRan, res_before, res_before};
+                stop = kSolveBudget;
+                ++cyc;
+                break;
+            }
+            if (total + Meff > cs.hist_cap) break;  // history buffer full: pause
+            int status;
+            double S;
+            const int executed = cycle(Meff, cs.omegas_all + off, a.hist + total, status, S);
+            const double ra = executed > 0 ? sqrt(S) / a.baseline : res_before;
+            if (threadIdx.x == 0)
+                cs.recs[cyc] = SolveRec{level, Mfull, executed, status, res_before, ra};
+            total += executed;
+            if (status == kStatusDiverged) { stop = kSolveDiverged; ++cyc; break; }
+            if (ra <= a.tol) { stop = kSolveConverged; res_before = ra; ++cyc; break; }
+            if (total >= cs.budget) { stop = kSolveBudget; res_before = ra; ++cyc; break; }
+            if (executed > 0 && res_before > 0.0 && ra > 0.0) prev = ra / res_before;
+            if (cs.mode == kSolveHeuristic) {
+                if (isfinite(prev)) level = heuristic_level(prev, level, cs.t_hi, cs.t_lo, cs.n_levels - 1);
+            } else if (cs.mode == kSolveIncreasing) {
+                level = min(level + 1, cs.n_levels - 1);
+            }
+            res_before = ra;
+        }
 #pragma unroll
         for (int j = 0; j < P; ++j)
-            if (FULL || i0 + j < n) dst[i0 + j] = x[j];
-    }
-    if (threadIdx.x == 0) {
-        a.out_i[0] = executed;
-        a.out_i[1] = status;
-        a.out_i[2] = executed & 1;
-        a.out_d[0] = S;
-        a.out_d[1] = sqrt(S) / a.baseline;
+            if (FULL || i0 + j < n) const_cast<double*>(a.xa)[i0 + j] = x[j];
+        if (threadIdx.x == 0) {
+            a.out_i[0] = cyc;
+            a.out_i[1] = stop;
+            a.out_i[2] = 0;
+            a.out_i[3] = level;
+            a.out_d[0] = res_before;
+            a.out_d[1] = prev;
+            a.out_d[2] = (double)total;
+        }
     }
 }
 
@@ -503,6 +574,11 @@ struct srj_op {
     double* slot_part[kSlots] = {nullptr, nullptr};
     unsigned* slot_counter = nullptr;  // device [kSlots], zero between launches
     int slot_capacity = 0;             // doubles per slot_part
+    // device-resident solve (srj_solve): per-cycle records and sweep history
+    SolveRec* solve_recs = nullptr;
+    int solve_recs_cap = 0;
+    double* solve_hist = nullptr;
+    long long solve_hist_cap = 0;
 };
 
 template <int FAM>
@@ -691,7 +767,10 @@ int srj_op_destroy(srj_op* op) {
     cudaFreeHost(op->h_hist);
     for (int s = 0; s < kSlots; ++s) cudaFree(op->slot_part[s]);
     cudaFree(op->slot_counter);
+    cudaFree(op->solve_recs);
+    cudaFree(op->solve_hist);
     plan2d_free(op->p2);
+    tbv_plan_free(op->tbv);
     delete op;
     return SRJ_OK;
 }
@@ -775,8 +854,8 @@ static int launch_cycle(srj_op* op, const double* xa, double* xb, const double* 
         const bool full = op->g.nx == per * 32 * kReg1dWarps;
         const dim3 grid(1), block(32 * kReg1dWarps);
 #define SRJ_REG1D(PP)                                                          \
-    if (full) k_reg_cycle_1d<PP, true><<<grid, block, 0, st>>>(a);            \
-    else k_reg_cycle_1d<PP, false><<<grid, block, 0, st>>>(a)
+    if (full) k_reg_cycle_1d<PP, true, false><<<grid, block, 0, st>>>(a);     \
+    else k_reg_cycle_1d<PP, false, false><<<grid, block, 0, st>>>(a)
         if (per <= 2) { SRJ_REG1D(2); }
         else if (per <= 4) { SRJ_REG1D(4); }
         else if (per <= 8) { SRJ_REG1D(8); }
@@ -885,6 +964,125 @@ int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
     out->res_after = op->h_out_d[1];
     if (history_host && executed > 0)
         std::memcpy(history_host, op->h_hist + 1, executed * sizeof(double));
+    return SRJ_OK;
+}
+
+// Which cycle kernel a device-resident solve runs on (0: none): the
+// temporally blocked kernels, whose cycles share one driver (srj_tbdriver.cuh),
+// and the register-resident 1D kernel.
+static int solve_kernel(const srj_op* op) {
+    if (reg1d_ok(op->g)) return SRJ_KERNEL_REG1D;
+    if (op->sweeps_per_pass <= 1) return 0;
+    if (op->tbv.supported) return SRJ_KERNEL_TBVAR;
+    if (op->tb3.supported) return SRJ_KERNEL_TB3D;
+    if (op->tb_kind == SRJ_TB_WARP_STREAM && op->ws.supported) return 0;
+    if (op->tb.supported) return SRJ_KERNEL_TB2D;
+    return 0;
+}
+
+int srj_op_solve_supported(const srj_op* op) { return op && solve_kernel(op) != 0 ? 1 : 0; }
+
+int srj_solve(srj_op* op, double* x, double* x_alt, const double* b, const srj_solve_args* args,
+              double tol, double baseline, srj_solve_rec* recs_host, double* history_host,
+              srj_solve_out* out, void* stream) {
+    if (!op || !x || !x_alt || !b || !args || !recs_host || !out)
+        return fail(SRJ_BAD_ARGUMENT, "null argument");
+    const int kern = solve_kernel(op);
+    if (!kern) return fail(SRJ_BAD_ARGUMENT, "no device-resident solve for this operator");
+    if (!args->omegas_all || !args->level_off || args->n_levels < 1 || args->max_cycles < 1 ||
+        args->level0 < 0 || args->level0 >= args->n_levels || args->mode < 0 || args->mode > 2)
+        return fail(SRJ_BAD_ARGUMENT, "bad solve arguments");
+    if (!(baseline > 0.0)) return fail(SRJ_BAD_ARGUMENT, "baseline must be positive");
+    if (args->hist_cap < kMaxSchemeLength) return fail(SRJ_BAD_ARGUMENT, "history capacity too small");
+    DeviceGuard guard(op->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e;
+    const int max_cycles = std::min(args->max_cycles, 4096);
+    if (op->solve_recs_cap < max_cycles) {
+        cudaFree(op->solve_recs);
+        op->solve_recs = nullptr;
+        op->solve_recs_cap = 0;
+        if ((e = cudaMalloc(&op->solve_recs, max_cycles * sizeof(SolveRec))) != cudaSuccess)
+            return fail(SRJ_CUDA_ERROR, std::string("allocation failed: ") + cudaGetErrorString(e));
+        op->solve_recs_cap = max_cycles;
+    }
+    const long long hist_cap = std::min<long long>(args->hist_cap, 1ll << 22);
+    if (op->solve_hist_cap < hist_cap) {
+        cudaFree(op->solve_hist);
+        op->solve_hist = nullptr;
+        op->solve_hist_cap = 0;
+        if ((e = cudaMalloc(&op->solve_hist, (hist_cap + 1) * sizeof(double))) != cudaSuccess)
+            return fail(SRJ_CUDA_ERROR, std::string("allocation failed: ") + cudaGetErrorString(e));
+        op->solve_hist_cap = hist_cap;
+    }
+    static_assert(sizeof(SolveRec) == sizeof(srj_solve_rec), "srj_solve_rec layout");
+    SolveCtl c;
+    c.omegas_all = args->omegas_all;
+    c.level_off = args->level_off;
+    c.n_levels = args->n_levels;
+    c.mode = args->mode;
+    c.level0 = args->level0;
+    c.max_cycles = max_cycles;
+    c.t_hi = args->t_hi;
+    c.t_lo = args->t_lo;
+    c.res0 = args->res0;
+    c.prev_ratio0 = args->prev_ratio0;
+    c.budget = args->budget;
+    c.hist_cap = hist_cap;
+    c.recs = op->solve_recs;
+    const Geom& g = op->g;
+    if (kern == SRJ_KERNEL_REG1D) {
+        CycleArgs a = {};
+        a.g = g;
+        a.xa = x;
+        a.xb = x_alt;
+        a.b = b;
+        a.tol = tol;
+        a.baseline = baseline;
+        a.hist = op->solve_hist;
+        a.out_i = op->out_i;
+        a.out_d = op->out_d;
+        a.ctl = c;
+        const int per = (g.nx + 32 * kReg1dWarps - 1) / (32 * kReg1dWarps);
+        const bool full = g.nx == per * 32 * kReg1dWarps;
+#define SRJ_REG1D_SOLVE(PP)                                                           \
+    if (full) k_reg_cycle_1d<PP, true, true><<<1, 32 * kReg1dWarps, 0, st>>>(a);     \
+    else k_reg_cycle_1d<PP, false, true><<<1, 32 * kReg1dWarps, 0, st>>>(a)
+        if (per <= 2) { SRJ_REG1D_SOLVE(2); }
+        else if (per <= 4) { SRJ_REG1D_SOLVE(4); }
+        else if (per <= 8) { SRJ_REG1D_SOLVE(8); }
+        else { SRJ_REG1D_SOLVE(16); }
+#undef SRJ_REG1D_SOLVE
+        CUDA_TRY(cudaGetLastError());
+    } else if (kern == SRJ_KERNEL_TBVAR)
+        CUDA_TRY(tbv_launch_cycle(op->tbv, g, x, x_alt, b, nullptr, 0, op->sweeps_per_pass, tol,
+                                  baseline, op->partials, op->solve_hist, op->out_i, op->out_d, st,
+                                  0, g.ny, nullptr, &c));
+    else if (kern == SRJ_KERNEL_TB3D)
+        CUDA_TRY(tb3_launch_cycle(op->tb3, g, x, x_alt, b, nullptr, 0, tol, baseline, op->partials,
+                                  op->solve_hist, op->out_i, op->out_d, st, 0, g.nz, nullptr, &c));
+    else
+        CUDA_TRY(tb_launch_cycle(op->tb, g, x, x_alt, b, nullptr, 0, op->sweeps_per_pass, tol,
+                                 baseline, op->partials, op->solve_hist, op->out_i, op->out_d, st,
+                                 0, g.ny, nullptr, &c));
+    CUDA_TRY(cudaMemcpyAsync(op->h_out_i, op->out_i, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(op->h_out_d, op->out_d, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    const int cycles = op->h_out_i[0];
+    const long long sweeps = (long long)op->h_out_d[2];
+    if (cycles > 0)
+        CUDA_TRY(cudaMemcpy(recs_host, op->solve_recs, cycles * sizeof(SolveRec),
+                            cudaMemcpyDeviceToHost));
+    if (history_host && sweeps > 0)
+        CUDA_TRY(cudaMemcpy(history_host, op->solve_hist + 1, sweeps * sizeof(double),
+                            cudaMemcpyDeviceToHost));
+    out->cycles = cycles;
+    out->stop = op->h_out_i[1];
+    out->result_in_alt = op->h_out_i[2];
+    out->next_level = op->h_out_i[3];
+    out->res_next = op->h_out_d[0];
+    out->prev_ratio = op->h_out_d[1];
+    out->sweeps = sweeps;
     return SRJ_OK;
 }
 

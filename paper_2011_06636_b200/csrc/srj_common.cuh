@@ -21,6 +21,31 @@ constexpr int kStatusRan = 0;
 constexpr int kStatusConverged = 1;
 constexpr int kStatusDiverged = 2;
 
+// Device-resident solve (the host controller loop of solver.py:305-326 run on
+// the device between cycles).  The scheme of level l is
+// omegas_all[level_off[l] .. level_off[l+1]) (application order).
+enum SolveMode { kSolveHeuristic = 0, kSolveIncreasing = 1, kSolveFixed = 2 };
+// Why a device solve returned: paused (cycle cap or history buffer full; the
+// host continues), converged, diverged, iteration budget exhausted.
+enum SolveStop { kSolvePaused = 0, kSolveConverged = 1, kSolveDiverged = 2, kSolveBudget = 3 };
+
+struct SolveRec {          // one cycle (matches srj_solve_rec in include/srj.h)
+    int level, M, executed, status;
+    double res_before, res_after;
+};
+
+struct SolveCtl {
+    const double* omegas_all;  // device
+    const int* level_off;      // device, n_levels + 1 entries
+    int n_levels, mode, level0, max_cycles;
+    double t_hi, t_lo;
+    double res0;               // residual entering the first cycle
+    double prev_ratio0;        // last finite residual ratio so far (NaN: none)
+    long long budget;          // sweeps allowed (max_iterations - total so far)
+    long long hist_cap;        // hist holds relative residuals of sweeps 1..hist_cap
+    SolveRec* recs;            // device, max_cycles entries
+};
+
 // Operator geometry as the kernels see it.  The flat interior index is
 // k = i + nx*j + nx*ny*z (x fastest, reference problems.py:119-120,158-161);
 // buffers carry `plane` ghost elements before and after the interior.

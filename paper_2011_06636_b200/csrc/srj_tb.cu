@@ -325,7 +325,7 @@ __device__ __forceinline__ void tile_dispatch(int h, TileRegs<K>& R, const doubl
 template <int K, bool SLAB>
 __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm_in,
                                           const CUtensorMap* tm_b, double* __restrict__ xout,
-                                          int k0, int h, double (&acc)[tb2d::Cfg<K>::S],
+                                          const double* om, int h, double (&acc)[tb2d::Cfg<K>::S],
                                           bool accumulate, unsigned ownmask, uint32_t& phase,
                                           bool first_issued, uint32_t& na) {
     using C = tb2d::Cfg<K>;
@@ -379,9 +379,9 @@ __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm
         if (threadIdx.x == 0 && q + (int)gridDim.x < a.ntiles)
             tb2d_issue<K, SLAB>(a, tm_in, tm_b, q + gridDim.x);
         if (masked)
-            tile_dispatch<K, true>(h, R, a.omegas + k0, a.g, warp, lane, inmask, accmask, acc, na);
+            tile_dispatch<K, true>(h, R, om, a.g, warp, lane, inmask, accmask, acc, na);
         else
-            tile_dispatch<K, false>(h, R, a.omegas + k0, a.g, warp, lane, inmask, accmask, acc, na);
+            tile_dispatch<K, false>(h, R, om, a.g, warp, lane, inmask, accmask, acc, na);
         if (storemask) {
 #pragma unroll
             for (int v = 0; v < V; ++v) {
@@ -404,7 +404,7 @@ __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm
     }
 }
 
-template <int K, bool SLAB>
+template <int K, bool SLAB, bool SOLVE>
 __global__ void __launch_bounds__(tb2d::Cfg<K>::THREADS, 1) __maxnreg__(tb2d::Cfg<K>::MAXREG)
     k_tb2d_cycle(const __grid_constant__ CUtensorMap tm_x0,
                  const __grid_constant__ CUtensorMap tm_x1,
@@ -436,17 +436,20 @@ __global__ void __launch_bounds__(tb2d::Cfg<K>::THREADS, 1) __maxnreg__(tb2d::Cf
     }
     uint32_t phase = 0, na = 0;
     const CUtensorMap* const tmx[2] = {&tm_x0, &tm_x1};
-    tb_run_cycle<S, F2D, SLAB>(
-        a, (int)blockIdx.x < a.ntiles,
-        [&](int in, double* xout, int k0, int h, double (&acc)[S], bool accumulate, bool first) {
-            tb2d_pass<K, SLAB>(a, tmx[in], &tm_b, xout, k0, h, acc, accumulate, ownmask, phase, first,
-                         na);
-        },
-        [&](int in) { tb2d_issue<K, SLAB>(a, tmx[in], &tm_b, blockIdx.x); },
-        [&]() {
-            mbar_wait(L::bar(), phase);
-            phase ^= 1u;
-        });
+    auto pass = [&](int in, double* xout, const double* om, int h, double (&acc)[S],
+                    bool accumulate, bool first) __attribute__((always_inline)) {
+        tb2d_pass<K, SLAB>(a, tmx[in], &tm_b, xout, om, h, acc, accumulate, ownmask, phase, first,
+                           na);
+    };
+    auto issue = [&](int in) { tb2d_issue<K, SLAB>(a, tmx[in], &tm_b, blockIdx.x); };
+    auto drain = [&]() __attribute__((always_inline)) {
+        mbar_wait(L::bar(), phase);
+        phase ^= 1u;
+    };
+    if constexpr (SOLVE)
+        tb_run_solve<S, F2D>(a, (int)blockIdx.x < a.ntiles, pass, issue, drain);
+    else
+        tb_run_cycle<S, F2D, SLAB>(a, (int)blockIdx.x < a.ntiles, pass, issue, drain);
 }
 
 // ----------------------------------------------------------------------------
@@ -456,13 +459,16 @@ __global__ void __launch_bounds__(tb2d::Cfg<K>::THREADS, 1) __maxnreg__(tb2d::Cf
 template <int K>
 static cudaError_t setup_variant(int& per_sm) {
     using C = tb2d::Cfg<K>;
-    cudaError_t e = cudaFuncSetAttribute(k_tb2d_cycle<K, false>,
+    cudaError_t e = cudaFuncSetAttribute(k_tb2d_cycle<K, false, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_tb2d_cycle<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)C::SMEM);
+    e = cudaFuncSetAttribute(k_tb2d_cycle<K, true, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tb2d_cycle<K, false>,
+    e = cudaFuncSetAttribute(k_tb2d_cycle<K, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tb2d_cycle<K, false, false>,
                                                          C::THREADS, C::SMEM);
 }
 
@@ -516,8 +522,9 @@ static cudaError_t launch_variant(const TbPlan& plan, const Geom& g, TbArgs& a, 
     a.ntiles = a.tiles_x * ((a.row_hi - a.row_lo + C::TY - 1) / C::TY);
     const int blocks = std::max(1, std::min(plan.blocks[K], a.ntiles));
     void* args[] = {&m0, &m1, &mb, &a};
-    const void* kern = a.sums != nullptr ? (const void*)k_tb2d_cycle<K, true>
-                                         : (const void*)k_tb2d_cycle<K, false>;
+    const void* kern = a.sums != nullptr        ? (const void*)k_tb2d_cycle<K, true, false>
+                       : a.ctl.max_cycles > 0 ? (const void*)k_tb2d_cycle<K, false, true>
+                                              : (const void*)k_tb2d_cycle<K, false, false>;
     return cudaLaunchCooperativeKernel(kern, dim3(blocks), dim3(C::THREADS), args, C::SMEM, st);
 }
 
@@ -525,10 +532,11 @@ cudaError_t tb_launch_cycle(const TbPlan& plan, const Geom& g, double* x, double
                             const double* b, const double* omegas, int M, int s, double tol,
                             double baseline, double* partials, double* hist, int* out_i,
                             double* out_d, cudaStream_t st, int row_lo, int row_hi,
-                            double* sums) {
+                            double* sums, const SolveCtl* ctl) {
     if ((((uintptr_t)x | (uintptr_t)x_alt | (uintptr_t)b) & 15) != 0)
         return cudaErrorMisalignedAddress;
     TbArgs a;
+    a.ctl = ctl ? *ctl : SolveCtl{};
     a.g = g;
     a.buf0 = x;
     a.buf1 = x_alt;

@@ -26,6 +26,10 @@ cudaError_t tb_plan_init(TbPlan& plan, const Geom& g, int num_sms);
 // for s <= 4, K=1 (S=6 ring) for s = 5, 6.
 int tb_variant_for(const TbPlan& plan, int s);
 
+// ctl != nullptr (all three TB launchers): a device-resident solve from x
+// (srj_tbdriver.cuh tb_run_solve) instead of one cycle; M and omegas are then
+// unused, out_i = {cycles, stop, result buffer, next level}, out_d = {residual
+// entering the next cycle, last finite ratio, sweeps}.
 // Launch one cycle of M sweeps, s per pass (1 <= s <= kTbMaxSub; the 2D
 // kernel fuses at most 4 and clamps larger requests).  Same
 // outputs as the one-sweep cycle kernel: out_i = {executed, status, result
@@ -38,7 +42,7 @@ cudaError_t tb_launch_cycle(const TbPlan& plan, const Geom& g, double* x, double
                             const double* b, const double* omegas, int M, int s, double tol,
                             double baseline, double* partials, double* hist, int* out_i,
                             double* out_d, cudaStream_t st, int row_lo, int row_hi,
-                            double* sums);
+                            double* sums, const SolveCtl* ctl = nullptr);
 
 // 3D 7-point temporal blocking (srj_tb3d.cu): S = sweeps fused per pass.
 struct Tb3Plan {
@@ -59,7 +63,8 @@ cudaError_t tb3_plan_init(Tb3Plan& plan, const Geom& g, int num_sms);
 cudaError_t tb3_launch_cycle(const Tb3Plan& plan, const Geom& g, double* x, double* x_alt,
                              const double* b, const double* omegas, int M, double tol,
                              double baseline, double* partials, double* hist, int* out_i,
-                             double* out_d, cudaStream_t st, int z_lo, int z_hi, double* sums);
+                             double* out_d, cudaStream_t st, int z_lo, int z_hi, double* sums,
+                             const SolveCtl* ctl = nullptr);
 
 // 2D variable-coefficient temporal blocking (srj_tbvar.cu), up to 6 sweeps per pass.
 struct TbvPlan {
@@ -76,6 +81,6 @@ cudaError_t tbv_launch_cycle(const TbvPlan& plan, const Geom& g, double* x, doub
                              const double* b, const double* omegas, int M, int s, double tol,
                              double baseline, double* partials, double* hist, int* out_i,
                              double* out_d, cudaStream_t st, int row_lo, int row_hi,
-                             double* sums);
+                             double* sums, const SolveCtl* ctl = nullptr);
 
 }  // namespace srj

@@ -424,7 +424,7 @@ __device__ __forceinline__ void tb3_consume(const TbArgs& a, const Tb3Items& it,
     }
 }
 
-template <bool SLAB>
+template <bool SLAB, bool SOLVE>
 __global__ void __launch_bounds__(tb3d::THREADS, 1)
     k_tb3d_cycle(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant__ CUtensorMap tm_x1,
                  const __grid_constant__ CUtensorMap tm_b, TbArgs a, Tb3Items it) {
@@ -442,17 +442,17 @@ __global__ void __launch_bounds__(tb3d::THREADS, 1)
     __syncthreads();
     uint32_t ld = 0;
     const CUtensorMap* const tmx[2] = {&tm_x0, &tm_x1};
-    tb_run_cycle<S, F3D, SLAB, !SLAB>(
-        a, (int)blockIdx.x < it.items,
-        [&](int in, double* xout, int k0, int h, double (&acc)[S], bool accumulate, bool) {
-            if (h == 0)  // residual of the cycle's final iterate
-                tb3_consume<1>(a, it, tmx[in], &tm_b, nullptr, a.omegas, accumulate, acc, ld);
-            else if (h == 2)
-                tb3_consume<2>(a, it, tmx[in], &tm_b, xout, a.omegas + k0, accumulate, acc, ld);
-            else
-                tb3_consume<1>(a, it, tmx[in], &tm_b, xout, a.omegas + k0, accumulate, acc, ld);
-        },
-        [](int) {}, []() {});
+    auto pass = [&](int in, double* xout, const double* om, int h, double (&acc)[S],
+                    bool accumulate, bool) __attribute__((always_inline)) {
+        if (h == 2)
+            tb3_consume<2>(a, it, tmx[in], &tm_b, xout, om, accumulate, acc, ld);
+        else  // h = 1, or h = 0 (xout == nullptr): residual of the cycle's final iterate
+            tb3_consume<1>(a, it, tmx[in], &tm_b, xout, om, accumulate, acc, ld);
+    };
+    if constexpr (SOLVE)
+        tb_run_solve<S, F3D, true>(a, (int)blockIdx.x < it.items, pass, [](int) {}, []() {});
+    else
+        tb_run_cycle<S, F3D, SLAB, !SLAB>(a, (int)blockIdx.x < it.items, pass, [](int) {}, []() {});
 }
 
 // ----------------------------------------------------------------------------
@@ -475,10 +475,10 @@ static int tb3_choose_zc(int ntiles, int slots, int nz) {
     return std::max(1, std::min(best_zc, nz));
 }
 
-template <bool SLAB>
+template <bool SLAB, bool SOLVE>
 static cudaError_t tb3_attr() {
-    return cudaFuncSetAttribute(k_tb3d_cycle<SLAB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)tb3d::SMEM);
+    return cudaFuncSetAttribute(k_tb3d_cycle<SLAB, SOLVE>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb3d::SMEM);
 }
 
 cudaError_t tb3_plan_init(Tb3Plan& plan, const Geom& g, int num_sms) {
@@ -486,9 +486,11 @@ cudaError_t tb3_plan_init(Tb3Plan& plan, const Geom& g, int num_sms) {
     // TMA needs a 16-byte row pitch (even nx).
     if (g.fam != F3D || (g.nx & 1) || !tma_available()) return cudaSuccess;
     cudaError_t e;
-    if ((e = tb3_attr<false>()) != cudaSuccess || (e = tb3_attr<true>()) != cudaSuccess) return e;
+    if ((e = tb3_attr<false, false>()) != cudaSuccess || (e = tb3_attr<true, false>()) != cudaSuccess ||
+        (e = tb3_attr<false, true>()) != cudaSuccess)
+        return e;
     int per_sm = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tb3d_cycle<false>,
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tb3d_cycle<false, false>,
                                                            tb3d::THREADS, tb3d::SMEM)) != cudaSuccess)
         return e;
     if (per_sm < 1) return cudaSuccess;
@@ -507,7 +509,8 @@ cudaError_t tb3_plan_init(Tb3Plan& plan, const Geom& g, int num_sms) {
 cudaError_t tb3_launch_cycle(const Tb3Plan& plan, const Geom& g, double* x, double* x_alt,
                              const double* b, const double* omegas, int M, double tol,
                              double baseline, double* partials, double* hist, int* out_i,
-                             double* out_d, cudaStream_t st, int z_lo, int z_hi, double* sums) {
+                             double* out_d, cudaStream_t st, int z_lo, int z_hi, double* sums,
+                             const SolveCtl* ctl) {
     if ((((uintptr_t)x | (uintptr_t)x_alt | (uintptr_t)b) & 15) != 0)
         return cudaErrorMisalignedAddress;
     const long long plane = (long long)g.nx * g.ny;
@@ -521,6 +524,7 @@ cudaError_t tb3_launch_cycle(const Tb3Plan& plan, const Geom& g, double* x, doub
     if ((e = encode_volume_map(&mb, b, g.nx, g.ny, g.nz, tb3d::RX, tb3d::BROWS)) != cudaSuccess)
         return e;
     TbArgs a;
+    a.ctl = ctl ? *ctl : SolveCtl{};
     a.g = g;
     a.buf0 = x;
     a.buf1 = x_alt;
@@ -554,7 +558,9 @@ cudaError_t tb3_launch_cycle(const Tb3Plan& plan, const Geom& g, double* x, doub
     }
     const int blocks = std::max(1, std::min(plan.num_sms, it.items));
     void* args[] = {&m0, &m1, &mb, &a, &it};
-    const void* fn = sums ? (const void*)k_tb3d_cycle<true> : (const void*)k_tb3d_cycle<false>;
+    const void* fn = sums  ? (const void*)k_tb3d_cycle<true, false>
+                     : ctl ? (const void*)k_tb3d_cycle<false, true>
+                           : (const void*)k_tb3d_cycle<false, false>;
     return cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(tb3d::THREADS), args, tb3d::SMEM, st);
 }
 

@@ -241,7 +241,7 @@ __device__ __forceinline__ void tbv_dispatch(int h, TbvRegs& R, const double* om
 
 template <bool SLAB>
 __device__ __forceinline__ void tbv_pass(const TbvArgs& a, const CUtensorMap* tm_in,
-                                         const TbvMaps& m, double* __restrict__ xout, int k0,
+                                         const TbvMaps& m, double* __restrict__ xout, const double* om,
                                          int h, double (&acc)[tbv::Cfg::S], bool accumulate,
                                          unsigned ownmask, uint32_t& phase, bool first_issued,
                                          uint32_t& na) {
@@ -312,9 +312,9 @@ __device__ __forceinline__ void tbv_pass(const TbvArgs& a, const CUtensorMap* tm
         if (threadIdx.x == 0 && q + (int)gridDim.x < a.ntiles)
             tbv_issue<SLAB>(a, tm_in, m, q + gridDim.x);
         if (masked)
-            tbv_dispatch<true>(h, R, a.omegas + k0, warp, lane, inmask, accmask, acc, na);
+            tbv_dispatch<true>(h, R, om, warp, lane, inmask, accmask, acc, na);
         else
-            tbv_dispatch<false>(h, R, a.omegas + k0, warp, lane, inmask, accmask, acc, na);
+            tbv_dispatch<false>(h, R, om, warp, lane, inmask, accmask, acc, na);
         if (storemask) {
 #pragma unroll
             for (int v = 0; v < V; ++v) {
@@ -333,7 +333,7 @@ __device__ __forceinline__ void tbv_pass(const TbvArgs& a, const CUtensorMap* tm
     }
 }
 
-template <bool SLAB>
+template <bool SLAB, bool SOLVE>
 __global__ void __launch_bounds__(tbv::Cfg::THREADS, 1)
     k_tbvar_cycle(const __grid_constant__ TbvMaps m, TbvArgs a) {
     using C = tbv::Cfg;
@@ -364,16 +364,19 @@ __global__ void __launch_bounds__(tbv::Cfg::THREADS, 1)
     }
     uint32_t phase = 0, na = 0;
     const CUtensorMap* const tmx[2] = {&m.x0, &m.x1};
-    tb_run_cycle<S, F2DV, SLAB>(
-        a, (int)blockIdx.x < a.ntiles,
-        [&](int in, double* xout, int k0, int h, double (&acc)[S], bool accumulate, bool first) {
-            tbv_pass<SLAB>(a, tmx[in], m, xout, k0, h, acc, accumulate, ownmask, phase, first, na);
-        },
-        [&](int in) { tbv_issue<SLAB>(a, tmx[in], m, blockIdx.x); },
-        [&]() {
-            mbar_wait(L::bar(), phase);
-            phase ^= 1u;
-        });
+    auto pass = [&](int in, double* xout, const double* om, int h, double (&acc)[S],
+                    bool accumulate, bool first) __attribute__((always_inline)) {
+        tbv_pass<SLAB>(a, tmx[in], m, xout, om, h, acc, accumulate, ownmask, phase, first, na);
+    };
+    auto issue = [&](int in) { tbv_issue<SLAB>(a, tmx[in], m, blockIdx.x); };
+    auto drain = [&]() __attribute__((always_inline)) {
+        mbar_wait(L::bar(), phase);
+        phase ^= 1u;
+    };
+    if constexpr (SOLVE)
+        tb_run_solve<S, F2DV>(a, (int)blockIdx.x < a.ntiles, pass, issue, drain);
+    else
+        tb_run_cycle<S, F2DV, SLAB>(a, (int)blockIdx.x < a.ntiles, pass, issue, drain);
 }
 
 // inv[p] = 1 / (((c_w + c_e) + c_s) + c_n), the reference's diagonal and
@@ -399,14 +402,17 @@ cudaError_t tbv_plan_init(TbvPlan& plan, const Geom& g, int num_sms) {
     plan = TbvPlan();
     // TMA needs 16-byte row pitches: even nx (x, b, fy, inv; fx via a padded copy).
     if (g.fam != F2DV || (g.nx & 1) || !g.fx || !g.fy || !tma_available()) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(k_tbvar_cycle<false>,
+    cudaError_t e = cudaFuncSetAttribute(k_tbvar_cycle<false, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_tbvar_cycle<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)C::SMEM);
+    e = cudaFuncSetAttribute(k_tbvar_cycle<true, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_tbvar_cycle<false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tbvar_cycle<false>,
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tbvar_cycle<false, false>,
                                                            C::THREADS, C::SMEM)) != cudaSuccess)
         return e;
     if (per_sm < 1) return cudaSuccess;
@@ -440,7 +446,7 @@ cudaError_t tbv_launch_cycle(const TbvPlan& plan, const Geom& g, double* x, doub
                              const double* b, const double* omegas, int M, int s, double tol,
                              double baseline, double* partials, double* hist, int* out_i,
                              double* out_d, cudaStream_t st, int row_lo, int row_hi,
-                             double* sums) {
+                             double* sums, const SolveCtl* ctl) {
     using C = tbv::Cfg;
     if ((((uintptr_t)x | (uintptr_t)x_alt | (uintptr_t)b) & 15) != 0)
         return cudaErrorMisalignedAddress;
@@ -455,6 +461,7 @@ cudaError_t tbv_launch_cycle(const TbvPlan& plan, const Geom& g, double* x, doub
     if ((e = encode_field_map(&m.fy, g.fy, g.nx, g.ny + 1, C::RX, C::RY)) != cudaSuccess) return e;
     if ((e = encode_field_map(&m.inv, plan.inv, g.nx, g.ny, C::RX, C::RY)) != cudaSuccess) return e;
     TbvArgs a;
+    a.ctl = ctl ? *ctl : SolveCtl{};
     a.g = g;
     a.buf0 = x;
     a.buf1 = x_alt;
@@ -475,8 +482,9 @@ cudaError_t tbv_launch_cycle(const TbvPlan& plan, const Geom& g, double* x, doub
     a.ntiles = a.tiles_x * ((row_hi - row_lo + C::TY - 1) / C::TY);
     const int blocks = std::max(1, std::min(plan.blocks, a.ntiles));
     void* args[] = {&m, &a};
-    const void* kern = sums != nullptr ? (const void*)k_tbvar_cycle<true>
-                                       : (const void*)k_tbvar_cycle<false>;
+    const void* kern = sums != nullptr ? (const void*)k_tbvar_cycle<true, false>
+                       : ctl            ? (const void*)k_tbvar_cycle<false, true>
+                                        : (const void*)k_tbvar_cycle<false, false>;
     return cudaLaunchCooperativeKernel(kern, dim3(blocks), dim3(C::THREADS), args, C::SMEM, st);
 }
 

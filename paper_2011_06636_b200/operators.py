@@ -199,6 +199,27 @@ class DeviceOperator:
             _stream_handle(self.device)), "srj_run_cycle")
         return out
 
+    def solve_supported(self) -> bool:
+        """True when whole solves can run on the device (srj_solve)."""
+        return bool(_lib.lib().srj_op_solve_supported(self.handle))
+
+    def solve_device(self, x: Field, x_alt: Field, b: Field, omegas_all, level_off,
+                     mode: int, level0: int, t_hi: float, t_lo: float, res0: float,
+                     prev_ratio: float, budget: int, tol: float, baseline: float,
+                     max_cycles: int, hist_cap: int, history: np.ndarray | None):
+        """Device-resident solve from x (srj_solve): returns (SolveOut, records)."""
+        args = _lib.SolveArgs(omegas_all.data_ptr(), level_off.data_ptr(), int(level_off.numel() - 1),
+                              int(mode), int(level0), int(max_cycles), float(t_hi), float(t_lo),
+                              float(res0), float(prev_ratio), int(budget), int(hist_cap))
+        recs = (_lib.SolveRec * int(max_cycles))()
+        out = _lib.SolveOut()
+        hist_ptr = history.ctypes.data if history is not None else None
+        _lib.check(_lib.lib().srj_solve(
+            self.handle, x.ptr, x_alt.ptr, b.ptr, ctypes.byref(args), float(tol), float(baseline),
+            ctypes.cast(recs, ctypes.c_void_p), hist_ptr, ctypes.byref(out),
+            _stream_handle(self.device)), "srj_solve")
+        return out, recs[:out.cycles]
+
     def run_cycle_diffinf(self, x: Field, x_alt: Field, b: Field, omegas_dev, M: int,
                           tol: float, res_before: float | None, budget: int,
                           history: np.ndarray | None):

@@ -7,7 +7,9 @@ to M weighted-Jacobi sweeps in the scheme's application order, evaluates the
 stopping rule before every sweep on a device-reduced residual norm, and the
 host reads back one small struct (executed, status, res_after) -- plus the
 per-sweep residuals only when `record_history` is set.  Scheme selection
-(Heuristic / Increasing / FixedM / Jacobi / Cjm) stays on the host.
+(Heuristic / Increasing / FixedM / Jacobi / Cjm) stays on the host, except that
+for the temporally blocked kernels `solve` runs the Heuristic / Increasing /
+FixedM loop on the device (srj_solve) with the same decisions.
 
 Parity contract: identical scheme sequence, executed counts and
 iterates (bitwise) to the reference; residual norms differ from OpenBLAS ddot
@@ -188,6 +190,103 @@ class _OmegaCache:
 
 
 _OMEGAS = _OmegaCache()
+
+
+class _LevelTables:
+    """Ordered omegas of every scheme a device-resident solve may pick, resident
+    in HBM: levels 0..MAX_LEVEL concatenated (Heuristic, Increasing) or one
+    fixed scheme (FixedM), with int32 offsets (srj_solve_args)."""
+
+    def __init__(self):
+        self._cache: dict = {}
+
+    def get(self, schemes: tuple, device):
+        import torch
+        key = (str(device), tuple((s.M, s.omegas, s.application_order) for s in schemes))
+        t = self._cache.get(key)
+        if t is None:
+            om = [w for s in schemes for w in s.ordered_omegas()]
+            off = np.concatenate([[0], np.cumsum([s.M for s in schemes])]).astype(np.int32)
+            t = (torch.tensor(om, dtype=torch.float64, device=device),
+                 torch.tensor(off, dtype=torch.int32, device=device))
+            if len(self._cache) > 64:
+                self._cache.clear()
+            self._cache[key] = t
+        return t
+
+
+_LEVEL_TABLES = _LevelTables()
+_SOLVE_HIST_CAP = 1 << 20   # sweeps one srj_solve call may record (then it pauses)
+_SOLVE_MAX_CYCLES = 4096
+
+
+def _device_solve_ok(A, controller, stopping: StoppingRule, cycle_hook) -> bool:
+    return (cycle_hook is None and stopping.norm in (ABSOLUTE_L2, RELATIVE_L2)
+            and isinstance(controller, (Heuristic, Increasing, FixedM))
+            and isinstance(A, StencilOperator) and A.solve_supported())
+
+
+def _solve_on_device(A: StencilOperator, b: Field, x: Field, x_alt: Field, controller,
+                     stopping: StoppingRule, order_grid: int, record_history: bool,
+                     baseline: float, t0: float) -> SolveReport:
+    """solve_fields with the controller loop on the device (srj_solve): the
+    same cycles, levels, stopping and report as the host loop below, one
+    launch per solve instead of one per cycle."""
+    if isinstance(controller, FixedM):
+        schemes = (generate_srj_scheme(controller.M, order_grid),)
+        mode, t_hi, t_lo = _lib.SOLVE_FIXED, 0.0, 0.0
+    else:
+        schemes = tuple(scheme_for_level(l, order_grid) for l in range(MAX_LEVEL + 1))
+        if isinstance(controller, Heuristic):
+            mode, t_hi, t_lo = _lib.SOLVE_HEURISTIC, controller.t_hi, controller.t_lo
+        else:
+            mode, t_hi, t_lo = _lib.SOLVE_INCREASING, 0.0, 0.0
+    omegas_all, level_off = _LEVEL_TABLES.get(schemes, A.device)
+    # the first cycle's incoming residual, as the host loop computes it
+    res_now = math.sqrt(A.residual_sq(x, b)) / baseline
+    history: list[tuple[int, float]] = [(0, res_now)] if record_history else []
+    hist = np.empty(_SOLVE_HIST_CAP, dtype=np.float64) if record_history else None
+    cycles: list[CycleStats] = []
+    total, cycle_index, level, prev = 0, 0, 0, math.nan
+    while True:
+        out, recs = A.solve_device(x, x_alt, b, omegas_all, level_off, mode, level, t_hi, t_lo,
+                                   res_now, prev, stopping.max_iterations - total,
+                                   stopping.tolerance, baseline, _SOLVE_MAX_CYCLES,
+                                   _SOLVE_HIST_CAP, hist)
+        done = 0
+        for rec in recs:
+            scheme = schemes[rec.level]
+            executed = int(rec.executed)
+            if rec.status == _lib.CYCLE_DIVERGED:
+                raise SolveDivergedError({
+                    "cycle": cycle_index, "sweep": executed,
+                    "omega": scheme.ordered_omegas()[executed - 1],
+                    "level": scheme.level, "M": scheme.M,
+                })
+            if record_history:
+                history.extend((total + k + 1, float(hist[done + k])) for k in range(executed))
+            rb, ra = float(rec.res_before), float(rec.res_after)
+            if executed > 0:
+                if rb > 0.0 and ra > 0.0:
+                    rate = average_convergence_rate(rb, ra, executed)
+                else:
+                    rate = math.inf
+                cycles.append(CycleStats(
+                    cycle=cycle_index, level=scheme.level if scheme.level is not None else -1,
+                    M=scheme.M, executed=executed, residual_before=rb, residual_after=ra,
+                    average_rate=rate))
+            total += executed
+            done += executed
+            cycle_index += 1
+        if out.result_in_alt:
+            x, x_alt = x_alt, x
+        if out.stop != _lib.SOLVE_PAUSED:
+            break
+        level, res_now, prev = int(out.next_level), float(out.res_next), float(out.prev_ratio)
+    return SolveReport(
+        converged=out.stop == _lib.SOLVE_CONVERGED, total_iterations=total, cycles=cycles,
+        wall_time=time.perf_counter() - t0, x=x.interior, residual_history=history,
+    )
 
 
 def _require_device_operator(A) -> DeviceOperator:
@@ -400,11 +499,15 @@ def _like(template, x_dev):
 
 def solve_fields(A: StencilOperator, b: Field, x: Field, x_alt: Field, controller: Controller,
                  stopping: StoppingRule, order_grid: int = ORDER_GRID_SIZE,
-                 record_history: bool = True, cycle_hook=None) -> SolveReport:
+                 record_history: bool = True, cycle_hook=None,
+                 device_loop: bool = True) -> SolveReport:
     """`solve` on device-resident Fields (no staging): x holds x0 on entry and
     both x and x_alt are overwritten.  The report's x is a CUDA view of
     whichever buffer holds the final iterate.  `cycle_hook(stats)` is called
-    after every cycle (bench instrumentation)."""
+    after every cycle (bench instrumentation; forces the host loop).  Where the
+    operator supports it (srj_op_solve_supported) and the controller is
+    Heuristic / Increasing / FixedM, the controller loop runs on the device
+    (`device_loop`, srj_solve): one launch per solve, same report."""
     t0 = time.perf_counter()
     _l2_norm_parts(stopping.norm)
     baseline = 1.0
@@ -412,6 +515,9 @@ def solve_fields(A: StencilOperator, b: Field, x: Field, x_alt: Field, controlle
         baseline = math.sqrt(A.residual_sq(x, b))
         if baseline == 0.0:
             raise ValueError("initial residual is zero; relative norm undefined")
+    if device_loop and _device_solve_ok(A, controller, stopping, cycle_hook):
+        return _solve_on_device(A, b, x, x_alt, controller, stopping, order_grid, record_history,
+                                baseline, t0)
     state = SolverState(x=x.interior, level=0)
     cycles: list[CycleStats] = []
     converged = False
