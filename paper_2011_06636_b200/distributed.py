@@ -547,15 +547,26 @@ class TbSlabSolver(SlabSolver):
     """`solve` over temporally blocked slabs: per cycle, passes of up to
     `ghost` sweeps, each one deep ghost-row exchange plus one srj_tb_pass;
     the residual of x_M over the owned rows; one all-gather of the per-sweep
-    owned sums; the same stop / rollback protocol as SlabSolver."""
+    owned sums; the same stop / rollback protocol as SlabSolver.
 
-    def __init__(self, slabs: list[TbSlab], exchanger):
+    overlap (None: on for 2D, off for 3D): a pass of a slab with a neighbour is
+    split into an interior launch -- the owned rows at least `ghost` rows away
+    from every ghost row, which never read a ghost row -- issued while the
+    exchange is in flight, then one launch per boundary band of `ghost` rows
+    once it has arrived.  Iterates are identical either way; the per-sweep sums
+    are added interior + lower + upper (fixed order)."""
+
+    def __init__(self, slabs: list[TbSlab], exchanger, overlap: bool | None = None):
         super().__init__(slabs, exchanger, engine=None)
         g = slabs[0].ghost
         if any(s.count < g for s in slabs):
             raise ValueError(f"every slab needs at least {g} rows")
         self.ghost = g
         self._omega_cache = {}
+        if overlap is None:
+            overlap = slabs[0].layout.family != "3d7"
+        self.overlap = overlap
+        self._band_sums = None
 
     # -- data ---------------------------------------------------------------
     def load(self, b=None, x0=None, seed: int | None = None) -> None:
@@ -596,17 +607,52 @@ class TbSlabSolver(SlabSolver):
             self._omega_cache[key] = t
         return t
 
+    def _bands(self, s: TbSlab):
+        """(interior, [boundary bands]) owned row ranges of a split pass, or
+        None when the pass is not split."""
+        g = self.ghost
+        lo, hi = s.owned
+        a = lo + (g if s.g_lo else 0)
+        b = hi - (g if s.g_hi else 0)
+        if not self.overlap or (a == lo and b == hi) or b <= a:
+            return None
+        bands = ([(lo, a)] if a > lo else []) + ([(b, hi)] if b < hi else [])
+        return (a, b), bands
+
     def _passes(self, om, sums, k_end: int) -> None:
         """Sweeps 0 .. k_end-1 of the cycle in passes of <= ghost."""
+        torch = _torch()
         k = 0
         while k < k_end:
             h = min(self.ghost, k_end - k)
-            self._exchange_rows()
-            for s, sm in zip(self.slabs, sums):
-                lo, hi = s.owned
-                s.A.tb_pass(s.x, s.x_alt, s.b, om.data_ptr() + 8 * k, h, lo, hi,
-                            sm.data_ptr() + 8 * k)
-            self.launches += len(self.slabs)
+            split = [self._bands(s) for s in self.slabs]
+            if not any(split):
+                self._exchange_rows()
+                for s, sm in zip(self.slabs, sums):
+                    lo, hi = s.owned
+                    s.A.tb_pass(s.x, s.x_alt, s.b, om.data_ptr() + 8 * k, h, lo, hi,
+                                sm.data_ptr() + 8 * k)
+                self.launches += len(self.slabs)
+            else:
+                if self._band_sums is None:
+                    self._band_sums = [torch.zeros((3, 8), dtype=torch.float64,
+                                                   device=s.x.buf.device) for s in self.slabs]
+                handle = self.ex.start_rows(self.slabs, [s.x for s in self.slabs])
+                # interior rows: no ghost row is read, so they run under the exchange
+                for s, sm, sp, bs in zip(self.slabs, sums, split, self._band_sums):
+                    lo, hi = sp[0] if sp else s.owned
+                    dst = bs[0].data_ptr() if sp else sm.data_ptr() + 8 * k
+                    s.A.tb_pass(s.x, s.x_alt, s.b, om.data_ptr() + 8 * k, h, lo, hi, dst)
+                self.ex.finish(handle)
+                for s, sm, sp, bs in zip(self.slabs, sums, split, self._band_sums):
+                    if not sp:
+                        continue
+                    bs[1:].zero_()
+                    for i, (lo, hi) in enumerate(sp[1]):
+                        s.A.tb_pass(s.x, s.x_alt, s.b, om.data_ptr() + 8 * k, h, lo, hi,
+                                    bs[1 + i].data_ptr())
+                    sm[k:k + h] = (bs[0, :h] + bs[1, :h]) + bs[2, :h]
+                self.launches += sum(1 + (len(sp[1]) if sp else 0) for sp in split)
             for s in self.slabs:
                 s.swap()
             k += h

@@ -27,9 +27,10 @@ def _rows(rep):
              c.average_rate) for c in rep.cycles]
 
 
+@pytest.mark.parametrize("overlap", [True, False])
 @pytest.mark.parametrize("world", [1, 2, 3, 4])
 @pytest.mark.parametrize("name", CASES)
-def test_tb_row_slabs_match_reference(name, world):
+def test_tb_row_slabs_match_reference(name, world, overlap):
     import torch
 
     import paper_2011_06636_b200 as srj
@@ -43,7 +44,7 @@ def test_tb_row_slabs_match_reference(name, world):
         pytest.skip("slabs need at least TB_GHOST rows")
     slabs = local_tb_slabs(fam, (n, n), world, range(world), torch.device("cuda", 0),
                            face_x=fx, face_y=fy)
-    solver = TbSlabSolver(slabs, LocalTbExchanger(world))
+    solver = TbSlabSolver(slabs, LocalTbExchanger(world), overlap=overlap)
     solver.load(b=b)
     rule = srj.StoppingRule(c["norm"], c["tol"], c.get("max_iterations", 10**9))
     rep = solver.solve(srj.Heuristic(), rule, record_history=False)
@@ -94,9 +95,10 @@ def test_tb_pass_owned_rows_vs_oracle(family):
         assert all(math.isfinite(v) for v in sq)
 
 
+@pytest.mark.parametrize("overlap", [False, True])
 @pytest.mark.parametrize("world", [1, 2, 3, 4])
 @pytest.mark.parametrize("name", CASES_3D)
-def test_tb_z_slabs_match_reference(name, world):
+def test_tb_z_slabs_match_reference(name, world, overlap):
     import torch
 
     import paper_2011_06636_b200 as srj
@@ -111,7 +113,7 @@ def test_tb_z_slabs_match_reference(name, world):
         pytest.skip("slabs need at least TB3_GHOST planes")
     slabs = local_tb_slabs(fam, (n, n, n), world, range(world), torch.device("cuda", 0))
     assert all(s.A.describe()["cycle_kernel"] == 5 for s in slabs)
-    solver = TbSlabSolver(slabs, LocalTbExchanger(world))
+    solver = TbSlabSolver(slabs, LocalTbExchanger(world), overlap=overlap)
     solver.load(b=b)
     rule = srj.StoppingRule(c["norm"], c["tol"], c.get("max_iterations", 10**9))
     ctrl = c["controller"]
