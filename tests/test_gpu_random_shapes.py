@@ -30,11 +30,17 @@ def _oracle_sweeps(op, x, b, omegas, baseline):
 
 
 def _case(family, seed):
-    rng = np.random.default_rng(1000 * seed + {"1d3": 1, "2d5": 2, "2d5var": 3, "3d7": 4}[family])
+    rng = np.random.default_rng(1000 * seed + {"1d3": 1, "2d5": 2, "2d5var": 3, "3d7": 4,
+                                               "3d7big": 5}[family])
     if family == "1d3":
         dims = (int(rng.integers(1, 3000)),)
     elif family == "3d7":
         dims = tuple(int(v) for v in rng.integers(1, 70, 3))
+    elif family == "3d7big":
+        # several tiles in x (60 owned columns) and y (32 rows), z runs split
+        # into items, ny not a multiple of the warp rows
+        dims = (2 * int(rng.integers(31, 100)), int(rng.integers(33, 140)),
+                int(rng.integers(1, 40)))
     else:
         nx = int(rng.choice([int(rng.integers(1, 40)), int(rng.integers(40, 300))]))
         ny = int(rng.choice([1, int(rng.integers(1, 30)), int(rng.integers(30, 260))]))
@@ -43,13 +49,16 @@ def _case(family, seed):
 
 
 @pytest.mark.parametrize("seed", range(20))
-@pytest.mark.parametrize("family", ["1d3", "2d5", "2d5var", "3d7"])
+@pytest.mark.parametrize("family", ["1d3", "2d5", "2d5var", "3d7", "3d7big"])
 def test_random_shape_cycle_bitwise(family, seed):
     import torch
 
     import paper_2011_06636_b200 as srj
     from oracle import srj_oracle as O
+    if family == "3d7big" and seed >= 8:
+        pytest.skip("8 seeds of the larger 3D grids")
     rng, dims = _case(family, seed)
+    family = family.replace("big", "")
     dev = torch.device("cuda", 0)
     n = int(np.prod(dims))
     nx, ny, nz = (list(dims) + [1, 1])[:3]
