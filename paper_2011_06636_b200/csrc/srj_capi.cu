@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kSmall1dThreads) k_small_cycle_1d(CycleArgs a)
 // (the diagonal term is fma(p, -2, y): c_diag = -2 c_off exactly, see srj_tb.cu
 // for the identity and the leading "0 +"), residual norms are summed in a
 // fixed order.  FULL: n == 256 P (no held points past n).
-constexpr int kReg1dWarps = 8;
+constexpr int kReg1dWarps = 8;      // most warps (n <= 32 * 8 * 16 = 4096)
 constexpr int kReg1dBatch = 16;
 
 // The register kernel applies c_diag*x as -2*p (exact: c_diag = -2 c_off).
@@ -243,9 +243,17 @@ static bool reg1d_ok(const Geom& g) {
     return g.fam == F1D && g.nx <= 32 * kReg1dWarps * 16 && g.c_diag == -2.0 * g.c_off;
 }
 
-template <int P, bool FULL, bool SOLVE>
-__global__ void __launch_bounds__(32 * kReg1dWarps) k_reg_cycle_1d(CycleArgs a) {
-    constexpr int K = kReg1dBatch, NW = kReg1dWarps;
+// Warps of the register kernel for n points: 4 up to 2048 (one barrier among
+// fewer warps is cheaper: C1 3.56 -> 3.40 ms), else 8; points per lane P.
+static void reg1d_shape(int n, int& nw, int& per) {
+    nw = n <= 32 * 4 * 16 ? 4 : 8;
+    per = (n + 32 * nw - 1) / (32 * nw);
+    per = per <= 2 ? 2 : per <= 4 ? 4 : per <= 8 ? 8 : 16;
+}
+
+template <int NW, int P, bool FULL, bool SOLVE>
+__global__ void __launch_bounds__(32 * NW) k_reg_cycle_1d(CycleArgs a) {
+    constexpr int K = kReg1dBatch;
     __shared__ double edge[2][2][NW + 2];  // [parity][first|last][warp + 1]
     __shared__ double red[K][NW + 1];
     __shared__ double stop_sum;
@@ -473,6 +481,22 @@ __global__ void __launch_bounds__(32 * kReg1dWarps) k_reg_cycle_1d(CycleArgs a) 
             a.out_d[2] = (double)total;
         }
     }
+}
+
+template <bool SOLVE>
+static void reg1d_launch(int nw, int per, bool full, const CycleArgs& a, cudaStream_t st) {
+#define SRJ_REG1D(NWW, PP)                                                         \
+    if (full) k_reg_cycle_1d<NWW, PP, true, SOLVE><<<1, 32 * NWW, 0, st>>>(a);    \
+    else k_reg_cycle_1d<NWW, PP, false, SOLVE><<<1, 32 * NWW, 0, st>>>(a)
+    if (nw == 4) {
+        if (per == 2) { SRJ_REG1D(4, 2); }
+        else if (per == 4) { SRJ_REG1D(4, 4); }
+        else if (per == 8) { SRJ_REG1D(4, 8); }
+        else { SRJ_REG1D(4, 16); }
+    } else {
+        SRJ_REG1D(8, 16);
+    }
+#undef SRJ_REG1D
 }
 
 template <int FAM, int MODE>
@@ -850,17 +874,10 @@ static int launch_cycle(srj_op* op, const double* xa, double* xb, const double* 
     a.out_i = op->out_i;
     a.out_d = op->out_d;
     if (!diff && reg1d_ok(op->g)) {
-        const int per = (op->g.nx + 32 * kReg1dWarps - 1) / (32 * kReg1dWarps);
-        const bool full = op->g.nx == per * 32 * kReg1dWarps;
-        const dim3 grid(1), block(32 * kReg1dWarps);
-#define SRJ_REG1D(PP)                                                          \
-    if (full) k_reg_cycle_1d<PP, true, false><<<grid, block, 0, st>>>(a);     \
-    else k_reg_cycle_1d<PP, false, false><<<grid, block, 0, st>>>(a)
-        if (per <= 2) { SRJ_REG1D(2); }
-        else if (per <= 4) { SRJ_REG1D(4); }
-        else if (per <= 8) { SRJ_REG1D(8); }
-        else { SRJ_REG1D(16); }
-#undef SRJ_REG1D
+        int nw, per;
+        reg1d_shape(op->g.nx, nw, per);
+        const bool full = op->g.nx == per * 32 * nw;
+        reg1d_launch<false>(nw, per, full, a, st);
         CUDA_TRY(cudaGetLastError());
         return SRJ_OK;
     }
@@ -1043,16 +1060,9 @@ int srj_solve(srj_op* op, double* x, double* x_alt, const double* b, const srj_s
         a.out_i = op->out_i;
         a.out_d = op->out_d;
         a.ctl = c;
-        const int per = (g.nx + 32 * kReg1dWarps - 1) / (32 * kReg1dWarps);
-        const bool full = g.nx == per * 32 * kReg1dWarps;
-#define SRJ_REG1D_SOLVE(PP)                                                           \
-    if (full) k_reg_cycle_1d<PP, true, true><<<1, 32 * kReg1dWarps, 0, st>>>(a);     \
-    else k_reg_cycle_1d<PP, false, true><<<1, 32 * kReg1dWarps, 0, st>>>(a)
-        if (per <= 2) { SRJ_REG1D_SOLVE(2); }
-        else if (per <= 4) { SRJ_REG1D_SOLVE(4); }
-        else if (per <= 8) { SRJ_REG1D_SOLVE(8); }
-        else { SRJ_REG1D_SOLVE(16); }
-#undef SRJ_REG1D_SOLVE
+        int nw, per;
+        reg1d_shape(g.nx, nw, per);
+        reg1d_launch<true>(nw, per, g.nx == per * 32 * nw, a, st);
         CUDA_TRY(cudaGetLastError());
     } else if (kern == SRJ_KERNEL_TBVAR)
         CUDA_TRY(tbv_launch_cycle(op->tbv, g, x, x_alt, b, nullptr, 0, op->sweeps_per_pass, tol,
