@@ -164,6 +164,8 @@ def cpu_sample(family, n, seed, budget_s):
     import numpy as np
 
     from oracle import srj_oracle as O
+    # every host thread this process may run on (torchrun sets OMP_NUM_THREADS=1)
+    O.clib().oracle_set_threads(len(os.sched_getaffinity(0)))
     fx = fy = None
     if family == "2d5var":
         from paper_2011_06636_b200.problems import gaussian_field, harmonic_faces
@@ -550,7 +552,7 @@ def run_ours(args, rank, world, local):
         "clocks": clocks.summary(),
         "gpu_launches": launches,
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # N = 1 only (contract)
         line["cpu_baseline"] = cpu_sample(family, n, args.seed, args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line), flush=True)
