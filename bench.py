@@ -379,6 +379,11 @@ def run_slabs(args, rank, world, local):
         # counted by the slab solver over the timed steps (+ one RHS fill per step)
         "gpu_launches": int(launches_timed + args.steps),
     }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # N = 1 only (contract)
+        # the same stencil family on the oracle port; 3D samples a 512^3 cube
+        # (config 3 / the per-GPU point count of config 5)
+        line["cpu_baseline"] = cpu_sample(family, 512 if family == "3d7" else shape[0],
+                                          args.seed, args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
