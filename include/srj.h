@@ -224,6 +224,11 @@ typedef struct srj_solve_out {
 } srj_solve_out;
 
 int srj_op_solve_supported(const srj_op* op);
+/* Leave k SMs free in the temporally blocked kernels' persistent grids (default
+ * 0), e.g. for the NCCL kernels of a halo exchange that overlaps a slab pass
+ * (the persistent CTAs otherwise occupy every SM, so NCCL could not run
+ * concurrently). */
+int srj_op_set_reserved_sms(srj_op* op, int32_t k);
 int srj_solve(srj_op* op, double* x, double* x_alt, const double* b, const srj_solve_args* args,
               double tol, double baseline, srj_solve_rec* recs_host, double* history_host,
               srj_solve_out* out, void* stream);

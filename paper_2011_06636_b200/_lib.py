@@ -28,6 +28,7 @@ EXPORTED_SYMBOLS = (
     "srj_run_cycle", "srj_sweep", "srj_matvec", "srj_fill_uniform_rhs",
     "srj_op_planes", "srj_sweep_planes", "srj_run_cycle_diffinf", "srj_batch_cycles_1d",
     "srj_op_set_temporal_kernel", "srj_tb_pass", "srj_op_solve_supported", "srj_solve",
+    "srj_op_set_reserved_sms",
 )
 SOLVE_PAUSED, SOLVE_CONVERGED, SOLVE_DIVERGED, SOLVE_BUDGET = 0, 1, 2, 3
 SOLVE_HEURISTIC, SOLVE_INCREASING, SOLVE_FIXED = 0, 1, 2
@@ -131,6 +132,7 @@ def _declare(L):
     L.srj_tb_pass.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
                               c_int64, c_int64, c_void_p, c_void_p]
     L.srj_op_solve_supported.argtypes = [c_void_p]
+    L.srj_op_set_reserved_sms.argtypes = [c_void_p, c_int32]
     L.srj_solve.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, POINTER(SolveArgs), c_double,
                             c_double, c_void_p, c_void_p, POINTER(SolveOut), c_void_p]
     for name in EXPORTED_SYMBOLS:

@@ -997,6 +997,13 @@ static int solve_kernel(const srj_op* op) {
     return 0;
 }
 
+int srj_op_set_reserved_sms(srj_op* op, int32_t k) {
+    if (!op) return fail(SRJ_BAD_ARGUMENT, "null operator");
+    if (k < 0 || k >= op->num_sms) return fail(SRJ_BAD_ARGUMENT, "reserved SMs out of range");
+    op->tb.reserved = op->tbv.reserved = op->tb3.reserved = k;
+    return SRJ_OK;
+}
+
 int srj_op_solve_supported(const srj_op* op) { return op && solve_kernel(op) != 0 ? 1 : 0; }
 
 int srj_solve(srj_op* op, double* x, double* x_alt, const double* b, const srj_solve_args* args,

@@ -520,7 +520,7 @@ static cudaError_t launch_variant(const TbPlan& plan, const Geom& g, TbArgs& a, 
     if ((e = encode_field_map(&mb, b, g.nx, g.ny, C::RX, C::RY)) != cudaSuccess) return e;
     a.tiles_x = plan.tiles_x[K];
     a.ntiles = a.tiles_x * ((a.row_hi - a.row_lo + C::TY - 1) / C::TY);
-    const int blocks = std::max(1, std::min(plan.blocks[K], a.ntiles));
+    const int blocks = std::max(1, std::min(plan.blocks[K] - plan.reserved, a.ntiles));
     void* args[] = {&m0, &m1, &mb, &a};
     const void* kern = a.sums != nullptr        ? (const void*)k_tb2d_cycle<K, true, false>
                        : a.ctl.max_cycles > 0 ? (const void*)k_tb2d_cycle<K, false, true>

@@ -18,6 +18,7 @@ struct TbPlan {
     int ntiles[8] = {};
     int small_variant = -1;         // forced variant (SRJ_TB_VARIANT), -1: by sweeps per pass
     int occupancy = 0;              // min resident CTAs per SM over the variants
+    int reserved = 0;               // SMs left free (srj_op_set_reserved_sms)
 };
 
 // Decide whether the operator has a temporal-blocking kernel and size its grid.
@@ -51,6 +52,7 @@ struct Tb3Plan {
     int sweeps = 0;
     int zc = 0, items = 0;  // planes per work item, work items (tiles x z-runs)
     int num_sms = 0;
+    int reserved = 0;       // SMs left free (srj_op_set_reserved_sms)
 };
 
 cudaError_t tb3_plan_init(Tb3Plan& plan, const Geom& g, int num_sms);
@@ -73,6 +75,7 @@ struct TbvPlan {
     double* fx_pad = nullptr;  // fx with a 16-byte row pitch (nx + 2)
     int fx_pitch = 0;
     double* inv = nullptr;     // 1 / diagonal, precomputed (reference order)
+    int reserved = 0;          // SMs left free (srj_op_set_reserved_sms)
 };
 
 cudaError_t tbv_plan_init(TbvPlan& plan, const Geom& g, int num_sms);

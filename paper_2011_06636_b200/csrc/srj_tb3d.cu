@@ -556,7 +556,7 @@ cudaError_t tb3_launch_cycle(const Tb3Plan& plan, const Geom& g, double* x, doub
         it.zc = tb3_choose_zc(plan.ntiles, plan.num_sms, nzr);
         it.items = plan.ntiles * ((nzr + it.zc - 1) / it.zc);
     }
-    const int blocks = std::max(1, std::min(plan.num_sms, it.items));
+    const int blocks = std::max(1, std::min(plan.num_sms - plan.reserved, it.items));
     void* args[] = {&m0, &m1, &mb, &a, &it};
     const void* fn = sums  ? (const void*)k_tb3d_cycle<true, false>
                      : ctl ? (const void*)k_tb3d_cycle<false, true>

@@ -480,7 +480,7 @@ cudaError_t tbv_launch_cycle(const TbvPlan& plan, const Geom& g, double* x, doub
     a.sums = sums;
     a.tiles_x = plan.tiles_x;
     a.ntiles = a.tiles_x * ((row_hi - row_lo + C::TY - 1) / C::TY);
-    const int blocks = std::max(1, std::min(plan.blocks, a.ntiles));
+    const int blocks = std::max(1, std::min(plan.blocks - plan.reserved, a.ntiles));
     void* args[] = {&m, &a};
     const void* kern = sums != nullptr ? (const void*)k_tbvar_cycle<true, false>
                        : ctl            ? (const void*)k_tbvar_cycle<false, true>

@@ -544,6 +544,7 @@ class TorchTbExchanger(TorchExchanger):
 
 
 class TbSlabSolver(SlabSolver):
+    NCCL_SMS = 4  # SMs the pass kernels leave to NCCL when the exchange overlaps
     """`solve` over temporally blocked slabs: per cycle, passes of up to
     `ghost` sweeps, each one deep ghost-row exchange plus one srj_tb_pass;
     the residual of x_M over the owned rows; one all-gather of the per-sweep
@@ -567,6 +568,10 @@ class TbSlabSolver(SlabSolver):
             overlap = slabs[0].layout.family != "3d7"
         self.overlap = overlap
         self._band_sums = None
+        if overlap and isinstance(exchanger, TorchTbExchanger) and exchanger.world > 1:
+            # NCCL's P2P kernels need SMs while the interior launch runs
+            for s in slabs:
+                s.A.set_reserved_sms(self.NCCL_SMS)
 
     # -- data ---------------------------------------------------------------
     def load(self, b=None, x0=None, seed: int | None = None) -> None:

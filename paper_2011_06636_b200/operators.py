@@ -199,6 +199,10 @@ class DeviceOperator:
             _stream_handle(self.device)), "srj_run_cycle")
         return out
 
+    def set_reserved_sms(self, k: int) -> None:
+        """Leave k SMs free in the temporally blocked kernels (srj_op_set_reserved_sms)."""
+        _lib.check(_lib.lib().srj_op_set_reserved_sms(self.handle, int(k)), "srj_op_set_reserved_sms")
+
     def solve_supported(self) -> bool:
         """True when whole solves can run on the device (srj_solve)."""
         return bool(_lib.lib().srj_op_solve_supported(self.handle))

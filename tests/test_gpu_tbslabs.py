@@ -156,3 +156,25 @@ def test_tb3_pass_owned_planes_vs_oracle(dims, lo, hi):
         assert np.array_equal(got[lo * pl:hi * pl], xs[h][lo * pl:hi * pl]), h
         assert np.all(got[:lo * pl] == 123.0) and np.all(got[hi * pl:] == 123.0), h
         np.testing.assert_allclose(sums.cpu().numpy(), sq, rtol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["c2_64", "c4_64", "c3_32"])
+def test_tb_slabs_with_reserved_sms(name):
+    """Pass kernels that leave SMs free for NCCL (overlapped exchange on real
+    multi-GPU runs) give the same iterates."""
+    import torch
+
+    import paper_2011_06636_b200 as srj
+    from paper_2011_06636_b200.distributed import (LocalTbExchanger, TbSlabSolver,
+                                                   local_tb_slabs)
+    c = P.case(name)
+    fam, n, b, fx, fy = P.case_inputs(c)
+    shape = (n, n, n) if fam == "3d7" else (n, n)
+    slabs = local_tb_slabs(fam, shape, 2, range(2), torch.device("cuda", 0), face_x=fx, face_y=fy)
+    for s in slabs:
+        s.A.set_reserved_sms(100)
+    solver = TbSlabSolver(slabs, LocalTbExchanger(2), overlap=True)
+    solver.load(b=b)
+    rule = srj.StoppingRule(c["norm"], c["tol"], c.get("max_iterations", 10**9))
+    rep = solver.solve(srj.Heuristic(), rule, record_history=False)
+    P.assert_trace_matches(c, _rows(rep), rep.total_iterations, rep.converged, x=solver.gather())
