@@ -1,7 +1,7 @@
 """3D temporal blocking (srj_tb3d.cu) against the reference traces and the oracle.
 
-The 3D golden cases run with both cycle kernels (sweeps_per_pass 1, the
-default: the plane ring k_cycle3d; 2: the z-wavefront k_tb3d_cycle), and a
+The 3D golden cases run with both cycle kernels (sweeps_per_pass 1: the plane
+ring k_cycle3d; 2, the default: the z-wavefront k_tb3d_cycle), and a
 multi-tile, non-cubic grid is swept cycle by cycle against oracle sweeps with
 every stop position inside a pass (rollback) exercised.
 """
