@@ -69,6 +69,25 @@ struct Geom {
     const double* cinv;   // 1.0 / diagonal [n]
 };
 
+// 64-bit warp shuffles with the two 32-bit halves moved explicitly.  The
+// built-in double overloads let ptxas land the halves in crossed registers and
+// repair them with XOR swaps (3 LOP3 per shuffle; ~7% of the 2D TB kernel's
+// instructions).
+__device__ __forceinline__ double shfl_up_d(double v, unsigned d) {
+    int lo = __double2loint(v), hi = __double2hiint(v);
+    asm volatile("shfl.sync.up.b32 %0, %0, %2, 0, -1;\n\tshfl.sync.up.b32 %1, %1, %2, 0, -1;"
+                 : "+r"(lo), "+r"(hi)
+                 : "r"(d));
+    return __hiloint2double(hi, lo);
+}
+__device__ __forceinline__ double shfl_down_d(double v, unsigned d) {
+    int lo = __double2loint(v), hi = __double2hiint(v);
+    asm volatile("shfl.sync.down.b32 %0, %0, %2, 31, -1;\n\tshfl.sync.down.b32 %1, %1, %2, 31, -1;"
+                 : "+r"(lo), "+r"(hi)
+                 : "r"(d));
+    return __hiloint2double(hi, lo);
+}
+
 // max that propagates NaN (fmax would drop it): a NaN difference must read
 // as non-finite in the solution-difference norm.
 __device__ __forceinline__ double nanmax(double a, double b) {

@@ -208,8 +208,8 @@ __device__ __forceinline__ void tile_sweeps(TileRegs<K>& R, const double* omegas
         double pw[V], pe[V];  // p across the lane boundary
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            pw[v] = __shfl_up_sync(0xffffffffu, R.p[v][CW - 1], 1);
-            pe[v] = __shfl_down_sync(0xffffffffu, R.p[v][0], 1);
+            pw[v] = shfl_up_d(R.p[v][CW - 1], 1);
+            pe[v] = shfl_down_d(R.p[v][0], 1);
         }
         double hs[CW], hn[CW];  // p of the rows above / below this warp's rows
         double sq[4] = {0.0, 0.0, 0.0, 0.0};  // r^2 partial sums, one per group slot

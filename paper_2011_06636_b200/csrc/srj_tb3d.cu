@@ -305,8 +305,8 @@ __device__ __forceinline__ void tb3_step(const Tb3Pt& t, int s, uint32_t n, int 
         // ghost columns -1 / nx of x_{k0+1} enter only through the shuffles
         const double su = t.gup ? -0.0 : p1[v + 1][1];
         const double sd = t.gdown ? -0.0 : p1[v + 1][0];
-        const double pw = __shfl_up_sync(0xffffffffu, su, 1);
-        const double pe = __shfl_down_sync(0xffffffffu, sd, 1);
+        const double pw = shfl_up_d(su, 1);
+        const double pe = shfl_down_d(sd, 1);
 #pragma unroll
         for (int j = 0; j < CW; ++j) {
             const double y = DADD(i2.y[v][j], p1[v + 1][j]);

@@ -151,8 +151,8 @@ __device__ __forceinline__ void tbv_sweeps(TbvRegs& R, const double* omegas, int
         double old_up[CW];                 // old x of the row above the current one
         double old_r1[CW], old_rl[CW];     // old rows 1 and V-2 (for the edge rows)
         auto row = [&](int v, const double (&xs)[CW], const double (&xn)[CW]) {
-            const double xw = __shfl_up_sync(0xffffffffu, R.x[v][CW - 1], 1);
-            const double xe = __shfl_down_sync(0xffffffffu, R.x[v][0], 1);
+            const double xw = shfl_up_d(R.x[v][CW - 1], 1);
+            const double xe = shfl_down_d(R.x[v][0], 1);
             double iv[CW];
             ld2(iv, L::inv() + (warp * V + v) * RX + col);
             double xo[CW];
