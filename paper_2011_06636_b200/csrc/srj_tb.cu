@@ -189,7 +189,8 @@ struct TileRegs {
 template <int K, int H, bool MASKED>
 __device__ __forceinline__ void tile_sweeps(TileRegs<K>& R, const double* omegas, const Geom& g,
                                             int warp, int lane, unsigned inmask, unsigned accmask,
-                                            double (&acc)[tb2d::Cfg<K>::S], uint32_t& na) {
+                                            double (&acc)[tb2d::Cfg<K>::S], uint32_t& na,
+                                            uint32_t hb) {
     using C = tb2d::Cfg<K>;
     using L = TbLayout<K>;
     constexpr int V = C::V, CW = C::CW, RX = C::RX;
@@ -276,8 +277,8 @@ __device__ __forceinline__ void tile_sweeps(TileRegs<K>& R, const double* omegas
             mbar_wait(L::hbar(na & 1), (na >> 1) & 1);
             ++na;
         }
-        lds_cols<CW>(hs, L::bot(t) + warp * RX + col);        // bottom row of warp-1
-        lds_cols<CW>(hn, L::top(t) + (warp + 2) * RX + col);  // top row of warp+1
+        lds_cols<CW>(hs, L::bot(hb + t) + warp * RX + col);        // bottom row of warp-1
+        lds_cols<CW>(hn, L::top(hb + t) + (warp + 2) * RX + col);  // top row of warp+1
         group(0, V - 1);
         if constexpr (!MASKED && kAligned)
             acc[t] = accmask != 0u ? DADD(acc[t], DADD(DADD(sq[0], sq[1]), DADD(sq[2], sq[3])))
@@ -289,8 +290,8 @@ __device__ __forceinline__ void tile_sweeps(TileRegs<K>& R, const double* omegas
 #pragma unroll
             for (int j = 0; j < CW; ++j) R.p[v][j] = DMUL(coff, R.x[v][j]);
         if (t + 1 < H) {
-            sts_cols<CW>(L::top(t + 1) + (warp + 1) * RX + col, R.p[0]);
-            sts_cols<CW>(L::bot(t + 1) + (warp + 1) * RX + col, R.p[V - 1]);
+            sts_cols<CW>(L::top(hb + t + 1) + (warp + 1) * RX + col, R.p[0]);
+            sts_cols<CW>(L::bot(hb + t + 1) + (warp + 1) * RX + col, R.p[V - 1]);
             __syncwarp();
             if (lane == 0) mbar_arrive(L::hbar(na & 1));
         }
@@ -301,12 +302,12 @@ template <int K, bool MASKED>
 __device__ __forceinline__ void tile_dispatch(int h, TileRegs<K>& R, const double* omegas,
                                               const Geom& g, int warp, int lane, unsigned inmask,
                                               unsigned accmask, double (&acc)[tb2d::Cfg<K>::S],
-                                              uint32_t& na) {
+                                              uint32_t& na, uint32_t hb) {
     constexpr int S = tb2d::Cfg<K>::S;
 #define SRJ_TB_CASE(H)                                                                      \
     case H:                                                                                 \
         if constexpr (H <= S)                                                               \
-            tile_sweeps<K, H, MASKED>(R, omegas, g, warp, lane, inmask, accmask, acc, na);  \
+            tile_sweeps<K, H, MASKED>(R, omegas, g, warp, lane, inmask, accmask, acc, na, hb); \
         break;
     switch (h) {
         SRJ_TB_CASE(1)
@@ -327,7 +328,7 @@ __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm
                                           const CUtensorMap* tm_b, double* __restrict__ xout,
                                           const double* om, int h, double (&acc)[tb2d::Cfg<K>::S],
                                           bool accumulate, unsigned ownmask, uint32_t& phase,
-                                          bool first_issued, uint32_t& na) {
+                                          bool first_issued, uint32_t& na, uint32_t& hb) {
     using C = tb2d::Cfg<K>;
     using L = TbLayout<K>;
     constexpr int S = C::S, V = C::V, CW = C::CW, RX = C::RX;
@@ -373,15 +374,16 @@ __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm
 #pragma unroll
             for (int j = 0; j < CW; ++j) R.p[v][j] = DMUL(coff, R.x[v][j]);
         }
-        sts_cols<CW>(L::top(0) + (warp + 1) * RX + c0, R.p[0]);
-        sts_cols<CW>(L::bot(0) + (warp + 1) * RX + c0, R.p[V - 1]);
+        sts_cols<CW>(L::top(hb) + (warp + 1) * RX + c0, R.p[0]);
+        sts_cols<CW>(L::bot(hb) + (warp + 1) * RX + c0, R.p[V - 1]);
         __syncthreads();  // stage consumed, halo rows published
         if (threadIdx.x == 0 && q + (int)gridDim.x < a.ntiles)
             tb2d_issue<K, SLAB>(a, tm_in, tm_b, q + gridDim.x);
         if (masked)
-            tile_dispatch<K, true>(h, R, om, a.g, warp, lane, inmask, accmask, acc, na);
+            tile_dispatch<K, true>(h, R, om, a.g, warp, lane, inmask, accmask, acc, na, hb);
         else
-            tile_dispatch<K, false>(h, R, om, a.g, warp, lane, inmask, accmask, acc, na);
+            tile_dispatch<K, false>(h, R, om, a.g, warp, lane, inmask, accmask, acc, na, hb);
+        hb += h;  // the next tile publishes into the parity after this tile's last
         if (storemask) {
 #pragma unroll
             for (int v = 0; v < V; ++v) {
@@ -398,9 +400,11 @@ __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm
                 }
             }
         }
-        // The halo rows of parity 0 are rewritten by the next tile: make sure
-        // every warp has finished reading this tile's last halos.
-        __syncthreads();
+        // No barrier here: the halo parity runs on across tiles (hb), so the
+        // next tile's first halo rows go to the buffer last read in sub-sweep
+        // h-2, which every warp had left before any warp passed the sub-sweep
+        // h-1 hand-off (h = 1: two tiles back, behind the next tile-start
+        // barrier).
     }
 }
 
@@ -434,12 +438,12 @@ __global__ void __launch_bounds__(tb2d::Cfg<K>::THREADS, 1) __maxnreg__(tb2d::Cf
                 if (c0 + j >= S && c0 + j < S + C::TX && r0 + v >= S && r0 + v < S + C::TY)
                     ownmask |= 1u << (v * C::CW + j);
     }
-    uint32_t phase = 0, na = 0;
+    uint32_t phase = 0, na = 0, hb = 0;
     const CUtensorMap* const tmx[2] = {&tm_x0, &tm_x1};
     auto pass = [&](int in, double* xout, const double* om, int h, double (&acc)[S],
                     bool accumulate, bool first) __attribute__((always_inline)) {
         tb2d_pass<K, SLAB>(a, tmx[in], &tm_b, xout, om, h, acc, accumulate, ownmask, phase, first,
-                           na);
+                           na, hb);
     };
     auto issue = [&](int in) { tb2d_issue<K, SLAB>(a, tmx[in], &tm_b, blockIdx.x); };
     auto drain = [&]() __attribute__((always_inline)) {
