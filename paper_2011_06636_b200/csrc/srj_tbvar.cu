@@ -54,7 +54,7 @@ struct Cfg {
     static constexpr int HBUF = 2 * HROWS * RX;    // top + bottom rows, one parity
     static constexpr int CSE = HROWS * RX;         // first-row c_s of every warp
     static constexpr size_t SMEM =
-        (size_t)(NST * STAGE + 2 * HBUF + CSE + STAGE) * sizeof(double) + 32;
+        (size_t)(NST * STAGE + 2 * HBUF + 2 * CSE + STAGE) * sizeof(double) + 32;
     static constexpr uint32_t TX_BYTES = NST * STAGE * sizeof(double);
 };
 
@@ -71,7 +71,7 @@ extern __shared__ __align__(128) double tbv_smem[];
 
 struct TbvLayout {
     using C = tbv::Cfg;
-    static constexpr int ST = 0, H = C::NST * C::STAGE, CSE = H + 2 * C::HBUF, INV = CSE + C::CSE,
+    static constexpr int ST = 0, H = C::NST * C::STAGE, CSE = H + 2 * C::HBUF, INV = CSE + 2 * C::CSE,
                          BAR = INV + C::STAGE;
     // stages: 0 x, 1 b, 2 c_w, 3 c_s, 4 inv
     __device__ static __forceinline__ double* st(int k) { return tbv_smem + ST + k * C::STAGE; }
@@ -79,7 +79,8 @@ struct TbvLayout {
     __device__ static __forceinline__ double* bot(int t) {
         return tbv_smem + H + (t & 1) * C::HBUF + C::HROWS * C::RX;
     }
-    __device__ static __forceinline__ double* cse() { return tbv_smem + CSE; }
+    // first-row c_s of every warp, double-buffered by tile parity
+    __device__ static __forceinline__ double* cse(int t) { return tbv_smem + CSE + (t & 1) * C::CSE; }
     // the tile's 1/diag, copied out of the stage (thread-private positions)
     __device__ static __forceinline__ double* inv() { return tbv_smem + INV; }
     __device__ static __forceinline__ uint64_t* bar() {
@@ -132,7 +133,7 @@ struct TbvRegs {
 template <int H, bool MASKED>
 __device__ __forceinline__ void tbv_sweeps(TbvRegs& R, const double* omegas, int warp, int lane,
                                            unsigned inmask, unsigned accmask,
-                                           double (&acc)[tbv::Cfg::S], uint32_t& na) {
+                                           double (&acc)[tbv::Cfg::S], uint32_t& na, uint32_t hb) {
     using C = tbv::Cfg;
     using L = TbvLayout;
     constexpr int V = C::V, CW = C::CW, RX = C::RX;
@@ -207,8 +208,8 @@ __device__ __forceinline__ void tbv_sweeps(TbvRegs& R, const double* omegas, int
             ++na;
         }
         double hs[CW], hn[CW];  // x of the rows above / below this warp's rows
-        ld2(hs, L::bot(t) + warp * RX + col);        // bottom row of warp-1
-        ld2(hn, L::top(t) + (warp + 2) * RX + col);  // top row of warp+1
+        ld2(hs, L::bot(hb + t) + warp * RX + col);        // bottom row of warp-1
+        ld2(hn, L::top(hb + t) + (warp + 2) * RX + col);  // top row of warp+1
         row(0, hs, old_r1);
         row(V - 1, old_rl, hn);
         if constexpr (!MASKED && kAligned)
@@ -216,8 +217,8 @@ __device__ __forceinline__ void tbv_sweeps(TbvRegs& R, const double* omegas, int
         else
             acc[t] = DADD(acc[t], DADD(sq[0], sq[1]));
         if (t + 1 < H) {
-            st2(L::top(t + 1) + (warp + 1) * RX + col, R.x[0]);
-            st2(L::bot(t + 1) + (warp + 1) * RX + col, R.x[V - 1]);
+            st2(L::top(hb + t + 1) + (warp + 1) * RX + col, R.x[0]);
+            st2(L::bot(hb + t + 1) + (warp + 1) * RX + col, R.x[V - 1]);
             __syncwarp();
             if (lane == 0) mbar_arrive(L::hbar(na & 1));
         }
@@ -227,14 +228,15 @@ __device__ __forceinline__ void tbv_sweeps(TbvRegs& R, const double* omegas, int
 template <bool MASKED>
 __device__ __forceinline__ void tbv_dispatch(int h, TbvRegs& R, const double* omegas, int warp,
                                              int lane, unsigned inmask, unsigned accmask,
-                                             double (&acc)[tbv::Cfg::S], uint32_t& na) {
+                                             double (&acc)[tbv::Cfg::S], uint32_t& na,
+                                             uint32_t hb) {
     switch (h) {
-        case 1: tbv_sweeps<1, MASKED>(R, omegas, warp, lane, inmask, accmask, acc, na); break;
-        case 2: tbv_sweeps<2, MASKED>(R, omegas, warp, lane, inmask, accmask, acc, na); break;
-        case 3: tbv_sweeps<3, MASKED>(R, omegas, warp, lane, inmask, accmask, acc, na); break;
-        case 4: tbv_sweeps<4, MASKED>(R, omegas, warp, lane, inmask, accmask, acc, na); break;
-        case 5: tbv_sweeps<5, MASKED>(R, omegas, warp, lane, inmask, accmask, acc, na); break;
-        case 6: tbv_sweeps<6, MASKED>(R, omegas, warp, lane, inmask, accmask, acc, na); break;
+        case 1: tbv_sweeps<1, MASKED>(R, omegas, warp, lane, inmask, accmask, acc, na, hb); break;
+        case 2: tbv_sweeps<2, MASKED>(R, omegas, warp, lane, inmask, accmask, acc, na, hb); break;
+        case 3: tbv_sweeps<3, MASKED>(R, omegas, warp, lane, inmask, accmask, acc, na, hb); break;
+        case 4: tbv_sweeps<4, MASKED>(R, omegas, warp, lane, inmask, accmask, acc, na, hb); break;
+        case 5: tbv_sweeps<5, MASKED>(R, omegas, warp, lane, inmask, accmask, acc, na, hb); break;
+        case 6: tbv_sweeps<6, MASKED>(R, omegas, warp, lane, inmask, accmask, acc, na, hb); break;
         default: break;
     }
 }
@@ -244,7 +246,7 @@ __device__ __forceinline__ void tbv_pass(const TbvArgs& a, const CUtensorMap* tm
                                          const TbvMaps& m, double* __restrict__ xout, const double* om,
                                          int h, double (&acc)[tbv::Cfg::S], bool accumulate,
                                          unsigned ownmask, uint32_t& phase, bool first_issued,
-                                         uint32_t& na) {
+                                         uint32_t& na, uint32_t& hb) {
     using C = tbv::Cfg;
     using L = TbvLayout;
     constexpr int S = C::S, V = C::V, CW = C::CW, RX = C::RX;
@@ -293,13 +295,13 @@ __device__ __forceinline__ void tbv_pass(const TbvArgs& a, const CUtensorMap* tm
             ld2(iv, L::st(4) + o);
             st2(L::inv() + o, iv);
         }
-        st2(L::top(0) + (warp + 1) * RX + c0, R.x[0]);
-        st2(L::bot(0) + (warp + 1) * RX + c0, R.x[V - 1]);
-        st2(L::cse() + (warp + 1) * RX + c0, R.cs[0]);
+        st2(L::top(hb) + (warp + 1) * RX + c0, R.x[0]);
+        st2(L::bot(hb) + (warp + 1) * RX + c0, R.x[V - 1]);
+        st2(L::cse(q / (int)gridDim.x) + (warp + 1) * RX + c0, R.cs[0]);
 #pragma unroll
         for (int v = 0; v < V; ++v) R.ce[v] = __shfl_down_sync(0xffffffffu, R.cw[v][0], 1);
         __syncthreads();  // stages consumed, edge rows published
-        ld2(R.cn, L::cse() + (warp + 2) * RX + c0);
+        ld2(R.cn, L::cse(q / (int)gridDim.x) + (warp + 2) * RX + c0);
         // diagonal once per tile (reference assembly order)
 #pragma unroll
         for (int v = 0; v < V; ++v)
@@ -312,9 +314,10 @@ __device__ __forceinline__ void tbv_pass(const TbvArgs& a, const CUtensorMap* tm
         if (threadIdx.x == 0 && q + (int)gridDim.x < a.ntiles)
             tbv_issue<SLAB>(a, tm_in, m, q + gridDim.x);
         if (masked)
-            tbv_dispatch<true>(h, R, om, warp, lane, inmask, accmask, acc, na);
+            tbv_dispatch<true>(h, R, om, warp, lane, inmask, accmask, acc, na, hb);
         else
-            tbv_dispatch<false>(h, R, om, warp, lane, inmask, accmask, acc, na);
+            tbv_dispatch<false>(h, R, om, warp, lane, inmask, accmask, acc, na, hb);
+        hb += h;  // the next tile publishes into the parity after this tile's last
         if (storemask) {
 #pragma unroll
             for (int v = 0; v < V; ++v) {
@@ -328,8 +331,8 @@ __device__ __forceinline__ void tbv_pass(const TbvArgs& a, const CUtensorMap* tm
                     row[1] = R.x[v][1];
             }
         }
-        // edge rows / first-row faces of parity 0 are rewritten by the next tile
-        __syncthreads();
+        // No barrier here: the halo parity runs on across tiles (hb) and the
+        // first-row faces alternate by tile (see srj_tb.cu tb2d_pass).
     }
 }
 
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(tbv::Cfg::THREADS, 1)
     using C = tbv::Cfg;
     using L = TbvLayout;
     constexpr int S = C::S;
-    for (int i = threadIdx.x; i < 2 * C::HBUF + C::CSE; i += blockDim.x) L::top(0)[i] = 0.0;
+    for (int i = threadIdx.x; i < 2 * C::HBUF + 2 * C::CSE; i += blockDim.x) L::top(0)[i] = 0.0;
     if (threadIdx.x == 0) {
         mbar_init(L::bar(), 1);
         mbar_init(L::hbar(0), C::NSEG);
@@ -362,11 +365,11 @@ __global__ void __launch_bounds__(tbv::Cfg::THREADS, 1)
                 if (c0 + j >= S && c0 + j < S + C::TX && r0 + v >= S && r0 + v < S + C::TY)
                     ownmask |= 1u << (v * C::CW + j);
     }
-    uint32_t phase = 0, na = 0;
+    uint32_t phase = 0, na = 0, hb = 0;
     const CUtensorMap* const tmx[2] = {&m.x0, &m.x1};
     auto pass = [&](int in, double* xout, const double* om, int h, double (&acc)[S],
                     bool accumulate, bool first) __attribute__((always_inline)) {
-        tbv_pass<SLAB>(a, tmx[in], m, xout, om, h, acc, accumulate, ownmask, phase, first, na);
+        tbv_pass<SLAB>(a, tmx[in], m, xout, om, h, acc, accumulate, ownmask, phase, first, na, hb);
     };
     auto issue = [&](int in) { tbv_issue<SLAB>(a, tmx[in], m, blockIdx.x); };
     auto drain = [&]() __attribute__((always_inline)) {
