@@ -132,6 +132,10 @@ struct TbLayout {
     __device__ static __forceinline__ uint64_t* hbar(int i) {
         return reinterpret_cast<uint64_t*>(tb_smem + BAR) + 1 + i;
     }
+    // stage consumed (one arrival per warp): the next tile's copy may start
+    __device__ static __forceinline__ uint64_t* sempty() {
+        return reinterpret_cast<uint64_t*>(tb_smem + BAR) + 3;
+    }
 };
 
 // CW contiguous doubles at a 16-byte aligned shared address.
@@ -273,7 +277,7 @@ __device__ __forceinline__ void tile_sweeps(TileRegs<K>& R, const double* omegas
 #pragma unroll
         for (int v = 1; v + 1 < V - 1; v += 2) group(v, v + 1);
         if ((V - 2) & 1) group(V - 2, -1);
-        if (t > 0) {  // halos of sub-sweep t were published by every warp
+        {  // halos of sub-sweep t were published by every warp (t = 0: at tile start)
             mbar_wait(L::hbar(na & 1), (na >> 1) & 1);
             ++na;
         }
@@ -328,7 +332,8 @@ __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm
                                           const CUtensorMap* tm_b, double* __restrict__ xout,
                                           const double* om, int h, double (&acc)[tb2d::Cfg<K>::S],
                                           bool accumulate, unsigned ownmask, uint32_t& phase,
-                                          bool first_issued, uint32_t& na, uint32_t& hb) {
+                                          bool first_issued, uint32_t& na, uint32_t& hb,
+                                          uint32_t& ne) {
     using C = tb2d::Cfg<K>;
     using L = TbLayout<K>;
     constexpr int S = C::S, V = C::V, CW = C::CW, RX = C::RX;
@@ -376,9 +381,20 @@ __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm
         }
         sts_cols<CW>(L::top(hb) + (warp + 1) * RX + c0, R.p[0]);
         sts_cols<CW>(L::bot(hb) + (warp + 1) * RX + c0, R.p[V - 1]);
-        __syncthreads();  // stage consumed, halo rows published
-        if (threadIdx.x == 0 && q + (int)gridDim.x < a.ntiles)
-            tb2d_issue<K, SLAB>(a, tm_in, tm_b, q + gridDim.x);
+        // No block barrier: each warp reports the stage consumed and its first
+        // halo rows published (sub-sweep 0 waits for that round); warp 0
+        // starts the next tile's copy once every warp has read the stage.
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(L::sempty());
+            mbar_arrive(L::hbar(na & 1));
+        }
+        if (warp == 0 && q + (int)gridDim.x < a.ntiles) {
+            mbar_wait(L::sempty(), ne & 1);  // the whole warp waits (no lone spinner)
+            if (lane == 0) tb2d_issue<K, SLAB>(a, tm_in, tm_b, q + gridDim.x);
+            __syncwarp();
+        }
+        ++ne;
         if (masked)
             tile_dispatch<K, true>(h, R, om, a.g, warp, lane, inmask, accmask, acc, na, hb);
         else
@@ -422,6 +438,7 @@ __global__ void __launch_bounds__(tb2d::Cfg<K>::THREADS, 1) __maxnreg__(tb2d::Cf
         mbar_init(L::bar(), 1);
         mbar_init(L::hbar(0), C::NSEG);
         mbar_init(L::hbar(1), C::NSEG);
+        mbar_init(L::sempty(), C::NSEG);
         prefetch_tensormap(&tm_x0);
         prefetch_tensormap(&tm_x1);
         prefetch_tensormap(&tm_b);
@@ -438,12 +455,12 @@ __global__ void __launch_bounds__(tb2d::Cfg<K>::THREADS, 1) __maxnreg__(tb2d::Cf
                 if (c0 + j >= S && c0 + j < S + C::TX && r0 + v >= S && r0 + v < S + C::TY)
                     ownmask |= 1u << (v * C::CW + j);
     }
-    uint32_t phase = 0, na = 0, hb = 0;
+    uint32_t phase = 0, na = 0, hb = 0, ne = 0;
     const CUtensorMap* const tmx[2] = {&tm_x0, &tm_x1};
     auto pass = [&](int in, double* xout, const double* om, int h, double (&acc)[S],
                     bool accumulate, bool first) __attribute__((always_inline)) {
         tb2d_pass<K, SLAB>(a, tmx[in], &tm_b, xout, om, h, acc, accumulate, ownmask, phase, first,
-                           na, hb);
+                           na, hb, ne);
     };
     auto issue = [&](int in) { tb2d_issue<K, SLAB>(a, tmx[in], &tm_b, blockIdx.x); };
     auto drain = [&]() __attribute__((always_inline)) {
