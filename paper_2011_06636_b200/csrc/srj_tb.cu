@@ -15,9 +15,13 @@
 // live in registers for all S sub-sweeps.  Neighbours:
 //   west/east  -- registers, or a warp shuffle across the lane boundary;
 //   north/south -- registers, or the halo rows the warps above/below publish
-//                  in shared memory (double-buffered by sub-sweep parity; a
-//                  split mbarrier per sub-sweep: interior rows are computed
-//                  between a warp's arrival and its wait).
+//                  in shared memory (double-buffered by a halo parity that
+//                  runs on across tiles; a split mbarrier per sub-sweep:
+//                  interior rows are computed between a warp's arrival and
+//                  its wait).
+// No block-wide barrier inside a pass: a tile's first halo rows are one more
+// hand-off round, and a "stage consumed" mbarrier (one arrival per warp) tells
+// warp 0 when the next tile's copy may overwrite the stage.
 // Measured on B200 (tools/probe/rates_probe.cu): a 64-bit warp shuffle costs
 // ~1/3 of the shared-memory bandwidth an LDS.64 exchange needs, so the only
 // shared traffic left is the staging load and the halo rows.
