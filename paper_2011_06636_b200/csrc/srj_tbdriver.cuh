@@ -103,8 +103,25 @@ __device__ __forceinline__ TbCycleResult tb_cycle(const TbArgs& a, const int& M,
         pass(in, buf[in ^ 1], omegas + k0, h, acc, true, issued);
         issued = false;
         double* part = a.partials + (size_t)(phase++ & 1) * kTbMaxSub * nb;
-        block_sums<S>(acc, h, sh, red);
-        if (threadIdx.x < h) part[threadIdx.x * nb + blockIdx.x] = red[threadIdx.x];
+        {
+            // CTA sums of the h sub-sweeps: warp butterflies, then thread t < h
+            // adds the warps' values in warp order (one block barrier)
+            const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+            const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+            for (int t = 0; t < S; ++t) {
+                if (t < h) {
+                    const double v = warp_allsum(acc[t]);
+                    if (lane == 0) sh[wid * S + t] = v;
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x < h) {
+                double v = sh[threadIdx.x];
+                for (int q = 1; q < nw; ++q) v += sh[q * S + threadIdx.x];
+                part[threadIdx.x * nb + blockIdx.x] = v;
+            }
+        }
         grid_barrier();
         if constexpr (SLAB) {  // pass mode: raw sums, no decision, no tail
             reduce_partials_multi(part, nb, h, red);
@@ -129,7 +146,6 @@ __device__ __forceinline__ TbCycleResult tb_cycle(const TbArgs& a, const int& M,
             if (!isfinite(r.res)) { r.status = kStatusDiverged; stop_t = t; break; }
             if (r.res <= a.tol) { r.status = kStatusConverged; stop_t = t; break; }
         }
-        __syncthreads();  // red[] is reused below
         if (stop_t >= 0) {
             stopped = true;
             r.executed = k0 + stop_t;
