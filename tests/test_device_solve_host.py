@@ -155,3 +155,23 @@ def test_report_equals_oracle(case, pause, monkeypatch):
     assert np.array_equal(rep.x, ref.x)
     if pause and pause[0] == 1:
         assert A.launches >= len(rep.cycles)
+
+
+def test_divergence_raises_like_the_host_loop():
+    """A cycle with a non-finite residual ends the device loop; the host raises
+    SolveDivergedError with the reference's diagnostic keys (solver.py:235-239)."""
+    from paper_2011_06636_b200.solver import SolveDivergedError
+    op = O.stencil("1d3", 50)
+    b = np.full(op.n, 1e306)
+    A = FakeDeviceOp(op)
+    x = _Field(np.zeros(op.n))
+    rule = StoppingRule("absolute_l2", 1e-8, 10**9)
+    with pytest.raises(SolveDivergedError) as e:
+        solver._solve_on_device(A, _Field(b), x, _Field(np.zeros(op.n)), Heuristic(), rule, 512,
+                                True, 1.0, 0.0)
+    d = e.value.diagnostics
+    assert set(d) == {"cycle", "sweep", "omega", "level", "M"}
+    with pytest.raises(O.OracleDiverged) as ref:
+        O.Oracle(op, b).solve(np.zeros(op.n), controller="heuristic", tol=1e-8, relative=False)
+    # the oracle counts sweeps over the whole solve, the diagnostics per cycle
+    assert d["omega"] == ref.value.omega
