@@ -103,3 +103,24 @@ def test_device_loop_only_where_supported():
     _, r2 = _solve(c, True)
     assert r1.total_iterations == r2.total_iterations
     assert [s.level for s in r1.cycles] == [s.level for s in r2.cycles]
+
+
+@pytest.mark.parametrize("fam,dims", [("2d5", (64, 64)), ("1d3", (300,)), ("3d7", (24, 24, 24))])
+def test_device_loop_divergence_matches_host_loop(fam, dims):
+    """Overflowing iterates: both loops raise SolveDivergedError with the same
+    diagnostics (cycle, sweep, omega, level, M)."""
+    import torch
+
+    import paper_2011_06636_b200 as srj
+    from paper_2011_06636_b200.solver import SolveDivergedError, solve_fields
+    dev = torch.device("cuda", 0)
+    diag = []
+    for device_loop in (True, False):
+        A = srj.StencilOperator(fam, dims, device=dev)
+        b = A.field(np.full(A.n, 1e306))
+        rule = srj.StoppingRule("absolute_l2", 1e-8, 10**9)
+        with pytest.raises(SolveDivergedError) as e:
+            solve_fields(A, b, A.new_field(), A.new_field(), srj.Heuristic(), rule,
+                         record_history=False, device_loop=device_loop)
+        diag.append(e.value.diagnostics)
+    assert diag[0] == diag[1]
