@@ -222,72 +222,74 @@ __device__ __forceinline__ void tile_sweeps(TileRegs<K>& R, const double* omegas
         }
         double hs[CW], hn[CW];  // p of the rows above / below this warp's rows
         double sq[4] = {0.0, 0.0, 0.0, 0.0};  // r^2 partial sums, one per group slot
-        // Rows va and vb (vb < 0: va only), both columns, computed in lockstep
-        // so the independent dependency chains interleave (fp64 latency ~9
-        // clk on B200).  Neighbours are the OLD p (updated after all rows).
-        auto group = [&](int va, int vb) {
-            constexpr int NP = 4;
-            const int np = vb >= 0 ? 4 : 2;
+        // Up to four rows (-1: unused), both columns, computed in lockstep so
+        // the independent dependency chains interleave (fp64 latency ~9 clk on
+        // B200): the four interior rows as one group of 8 chains (2048^2 sweep
+        // 8.11 -> 7.96 us vs two groups of 4), then the two edge rows after the
+        // halo hand-off.  Neighbours are the OLD p (updated after all rows).
+        auto group = [&](int va, int vb, int vc, int vd) {
+            constexpr int NP = 8;
+            const int rows[4] = {va, vb, vc, vd};
+            const int np = vd >= 0 ? 8 : vc >= 0 ? 6 : vb >= 0 ? 4 : 2;
             double y[NP], rr[NP];
 #pragma unroll
             for (int k = 0; k < NP; ++k) {
                 if (k >= np) break;
-                const int v = k < 2 ? va : vb, j = k & 1;
+                const int v = rows[k >> 1], j = k & 1;
                 y[k] = v == 0 ? hs[j] : R.p[v - 1][j];  // 0 + p_s (see header)
             }
 #pragma unroll
             for (int k = 0; k < NP; ++k) {
                 if (k >= np) break;
-                const int v = k < 2 ? va : vb, j = k & 1;
+                const int v = rows[k >> 1], j = k & 1;
                 y[k] = DADD(y[k], j == 0 ? pw[v] : R.p[v][j - 1]);
             }
 #pragma unroll
             for (int k = 0; k < NP; ++k) {
                 if (k >= np) break;
-                const int v = k < 2 ? va : vb, j = k & 1;
+                const int v = rows[k >> 1], j = k & 1;
                 y[k] = __fma_rn(R.p[v][j], -4.0, y[k]);  // + c_diag*x = -4*p (see header)
             }
 #pragma unroll
             for (int k = 0; k < NP; ++k) {
                 if (k >= np) break;
-                const int v = k < 2 ? va : vb, j = k & 1;
+                const int v = rows[k >> 1], j = k & 1;
                 y[k] = DADD(y[k], j == CW - 1 ? pe[v] : R.p[v][j + 1]);
             }
 #pragma unroll
             for (int k = 0; k < NP; ++k) {
                 if (k >= np) break;
-                const int v = k < 2 ? va : vb, j = k & 1;
+                const int v = rows[k >> 1], j = k & 1;
                 y[k] = DADD(y[k], v == V - 1 ? hn[j] : R.p[v + 1][j]);
             }
 #pragma unroll
             for (int k = 0; k < NP; ++k) {
                 if (k >= np) break;
-                const int v = k < 2 ? va : vb, j = k & 1;
+                const int v = rows[k >> 1], j = k & 1;
                 rr[k] = DSUB(R.b[v][j], y[k]);
             }
 #pragma unroll
             for (int k = 0; k < NP; ++k) {
                 if (k >= np) break;
-                const int v = k < 2 ? va : vb, j = k & 1;
+                const int v = rows[k >> 1], j = k & 1;
                 const int bit = v * CW + j;
                 const double xn = relax(R.x[v][j], inv, rr[k], w);
                 if constexpr (!MASKED && kAligned)
-                    sq[k] = fma(rr[k], rr[k], sq[k]);  // owned: decided per thread below
+                    sq[k & 3] = fma(rr[k], rr[k], sq[k & 3]);  // owned: decided per thread below
                 else
-                    fma_sq_if(sq[k], rr[k], (accmask >> bit) & 1u);
+                    fma_sq_if(sq[k & 3], rr[k], (accmask >> bit) & 1u);
                 R.x[v][j] = (!MASKED || ((inmask >> bit) & 1u)) ? xn : 0.0;
             }
         };
-#pragma unroll
-        for (int v = 1; v + 1 < V - 1; v += 2) group(v, v + 1);
-        if ((V - 2) & 1) group(V - 2, -1);
+        static_assert(V == 6, "interior rows 1..4 form one group");
+        group(1, 2, 3, 4);
         {  // halos of sub-sweep t were published by every warp (t = 0: at tile start)
             mbar_wait(L::hbar(na & 1), (na >> 1) & 1);
             ++na;
         }
         lds_cols<CW>(hs, L::bot(hb + t) + warp * RX + col);        // bottom row of warp-1
         lds_cols<CW>(hn, L::top(hb + t) + (warp + 2) * RX + col);  // top row of warp+1
-        group(0, V - 1);
+        group(0, V - 1, -1, -1);
         if constexpr (!MASKED && kAligned)
             acc[t] = accmask != 0u ? DADD(acc[t], DADD(DADD(sq[0], sq[1]), DADD(sq[2], sq[3])))
                                    : acc[t];
