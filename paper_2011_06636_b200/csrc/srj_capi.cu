@@ -305,8 +305,9 @@ __global__ void __launch_bounds__(32 * NW) k_reg_cycle_1d(CycleArgs a) {
                 x[j] = (FULL || i0 + j < n) ? xn : 0.0;
                 p[j] = DMUL(c, x[j]);
             }
-            if (lane == 0) edge[par ^ 1][0][wid + 1] = p[0];
-            if (lane == 31) edge[par ^ 1][1][wid + 1] = p[P - 1];
+            // one predicated store (lanes 0 and 31), no divergent branch
+            if (lane == 0 || lane == 31)
+                edge[par ^ 1][lane == 31][wid + 1] = lane == 0 ? p[0] : p[P - 1];
             __syncthreads();
             par ^= 1;
         }
