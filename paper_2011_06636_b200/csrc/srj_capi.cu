@@ -331,10 +331,15 @@ __global__ void __launch_bounds__(32 * NW) k_reg_cycle_1d(CycleArgs a) {
             double v[K], wv[K];  // the batch's omegas, loaded up front (off the sweep chain)
 #pragma unroll
             for (int s = 0; s < K; ++s) wv[s] = (!tail && s < kk) ? __ldg(omegas + kb + s) : 0.0;
+            if (kk == K) {  // a full batch: no per-sweep guard (uniform, branch-free)
 #pragma unroll
-            for (int s = 0; s < K; ++s) {
-                v[s] = 0.0;
-                if (s < kk) v[s] = sweep(wv[s], !tail);
+                for (int s = 0; s < K; ++s) v[s] = sweep(wv[s], true);
+            } else {
+#pragma unroll
+                for (int s = 0; s < K; ++s) {
+                    v[s] = 0.0;
+                    if (s < kk) v[s] = sweep(wv[s], !tail);
+                }
             }
             // transposed butterfly: after the rounds lane l holds the warp sum of
             // sweep (l >> 1) & (K-1) (fixed order; both lanes of a pair agree)
