@@ -412,13 +412,10 @@ __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm
                 double* row = xout + (long long)(gy0 + v) * nx + gx0;
 #pragma unroll
                 for (int j = 0; j < CW; j += 2) {
-                    const unsigned m2 = (storemask >> (v * CW + j)) & 3u;
-                    if (m2 == 3u)
+                    // a lane's column pair is owned / inside the grid as a whole
+                    // (even nx, even ring and tile widths): one predicated store
+                    if ((storemask >> (v * CW + j)) & 1u)
                         *reinterpret_cast<double2*>(row + j) = make_double2(R.x[v][j], R.x[v][j + 1]);
-                    else if (m2 == 1u)
-                        row[j] = R.x[v][j];
-                    else if (m2 == 2u)
-                        row[j + 1] = R.x[v][j + 1];
                 }
             }
         }

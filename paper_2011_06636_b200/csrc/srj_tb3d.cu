@@ -163,13 +163,10 @@ struct Tb3Pt {
     long long rowoff;  // flat offset of grid row oy + r0, column gx0
 };
 
-__device__ __forceinline__ void st_row(double* row, double v0, double v1, bool o0, bool o1) {
-    if (o0 && o1)
-        *reinterpret_cast<double2*>(row) = make_double2(v0, v1);
-    else if (o0)
-        row[0] = v0;
-    else if (o1)
-        row[1] = v1;
+// A lane's column pair is owned / inside the grid as a whole (even nx, even
+// box origin and ring), so own0 == own1: one predicated 16-byte store.
+__device__ __forceinline__ void st_row(double* row, double v0, double v1, bool o0, bool) {
+    if (o0) *reinterpret_cast<double2*>(row) = make_double2(v0, v1);
 }
 
 // One plane step.  Level 1 reads plane z of x_{k0} from stage n, finishes
