@@ -322,13 +322,10 @@ __device__ __forceinline__ void tbv_pass(const TbvArgs& a, const CUtensorMap* tm
 #pragma unroll
             for (int v = 0; v < V; ++v) {
                 double* row = xout + (long long)(gy0 + v) * nx + gx0;
-                const unsigned m2 = (storemask >> (v * CW)) & 3u;
-                if (m2 == 3u)
+                // a lane's column pair is owned / inside the grid as a whole
+                // (even nx, even ring and tile widths): one predicated store
+                if ((storemask >> (v * CW)) & 1u)
                     *reinterpret_cast<double2*>(row) = make_double2(R.x[v][0], R.x[v][1]);
-                else if (m2 == 1u)
-                    row[0] = R.x[v][0];
-                else if (m2 == 2u)
-                    row[1] = R.x[v][1];
             }
         }
         // No barrier here: the halo parity runs on across tiles (hb) and the
