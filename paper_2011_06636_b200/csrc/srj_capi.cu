@@ -220,8 +220,9 @@ __global__ void __launch_bounds__(kSmall1dThreads) k_small_cycle_1d(CycleArgs a)
 
 // Register-resident 1D cycle (n <= 32 * kReg1dWarps * 16): NW warps (4 up to
 // n = 2048, else 8; reg1d_shape), lane l of warp w holds P consecutive points
-// [(32w + l) P, +P) -- x, b and p = c*x in registers for the whole cycle.  Neighbours inside a lane are registers, across
-// lanes one shuffle each way, across warps the edge p of the neighbouring warps
+// [(32w + l) P, +P) -- x, b and p = c*x in registers for the whole cycle.
+// Neighbours inside a lane are registers, across lanes one shuffle each way,
+// across warps the edge p of the neighbouring warps
 // through shared memory (double-buffered by sweep parity), one __syncthreads
 // per sweep.
 //
