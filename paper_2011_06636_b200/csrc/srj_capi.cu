@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kSmall1dThreads) k_small_cycle_1d(CycleArgs a)
 // for the identity and the leading "0 +"), residual norms are summed in a
 // fixed order.  FULL: n == 256 P (no held points past n).
 constexpr int kReg1dWarps = 8;      // most warps (n <= 32 * 8 * 16 = 4096)
-constexpr int kReg1dBatch = 16;
+constexpr int kReg1dBatch = 32;     // sweeps per stop-test batch (16 for P = 16: registers)
 
 // The register kernel applies c_diag*x as -2*p (exact: c_diag = -2 c_off).
 static bool reg1d_ok(const Geom& g) {
@@ -254,7 +254,7 @@ static void reg1d_shape(int n, int& nw, int& per) {
 
 template <int NW, int P, bool FULL, bool SOLVE>
 __global__ void __launch_bounds__(32 * NW) k_reg_cycle_1d(CycleArgs a) {
-    constexpr int K = kReg1dBatch;
+    constexpr int K = P <= 8 ? kReg1dBatch : 16;
     __shared__ double edge[2][2][NW + 2];  // [parity][first|last][warp + 1]
     __shared__ double red[K][NW + 1];
     __shared__ double stop_sum;
@@ -342,8 +342,11 @@ __global__ void __launch_bounds__(32 * NW) k_reg_cycle_1d(CycleArgs a) {
                     if (s < kk) v[s] = sweep(wv[s], !tail);
                 }
             }
-            // transposed butterfly: after the rounds lane l holds the warp sum of
-            // sweep (l >> 1) & (K-1) (fixed order; both lanes of a pair agree)
+            // transposed butterfly: log2(K) halving rounds (lane bits 16, 8, ...),
+            // then plain butterfly rounds over the remaining low lane bits; lane l
+            // ends with the warp sum of sweep (l / (32/K)) (fixed order; the lanes
+            // of a group agree)
+            constexpr int G = 32 / K;  // lanes per sweep after the halving rounds
 #pragma unroll
             for (int h = K / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
                 const bool hi = (lane & o) != 0;
@@ -354,8 +357,9 @@ __global__ void __launch_bounds__(32 * NW) k_reg_cycle_1d(CycleArgs a) {
                     v[i] = DADD(keep, __shfl_xor_sync(0xffffffffu, send, o));
                 }
             }
-            v[0] = DADD(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
-            if ((lane & 1) == 0) red[(lane >> 1) & (K - 1)][wid] = v[0];
+#pragma unroll
+            for (int o = G / 2; o >= 1; o >>= 1) v[0] = DADD(v[0], __shfl_xor_sync(0xffffffffu, v[0], o));
+            if ((lane & (G - 1)) == 0) red[lane / G][wid] = v[0];
             __syncthreads();
             if (wid == 0) {
                 // lane s: the residual of x_{kb+s}, warp partials in warp order
