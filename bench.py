@@ -78,7 +78,22 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SRJ_BENCH_SHARE_DEVICE=1 (checking only): every rank on cuda:0, so the
+    # N > 1 replica path (barriers, max over ranks, rank-0 line) runs on a
+    # one-GPU box; replicas never wait on one another.  Never a bench number.
+    if os.environ.get("SRJ_BENCH_SHARE_DEVICE") == "1":
+        local = 0
     return rank, world, local
+
+
+def init_dist(dev):
+    """One process per GPU over NCCL; SRJ_BENCH_BACKEND=gloo pairs with
+    SRJ_BENCH_SHARE_DEVICE for the one-GPU check of the N > 1 path."""
+    import torch.distributed as dist
+    if os.environ.get("SRJ_BENCH_BACKEND", "nccl") == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(os.environ["SRJ_BENCH_BACKEND"])
 
 
 class ClockSampler:
@@ -250,7 +265,7 @@ def run_slabs(args, rank, world, local):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dev)
     throughput = args.config == "c5"
     face_x = face_y = None
     if throughput:
@@ -405,7 +420,7 @@ def run_ours(args, rank, world, local):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dev)
     family, extent, _ = CONFIGS[args.config]
     n = args.size or extent
     prob = srj.baseline_problem(family, n, seed=args.seed, device=dev, rhs_on_device=True)
