@@ -75,3 +75,11 @@ def test_kernels_use_tma_and_no_fma_in_the_stencil():
     sass = out.stdout
     assert "UTMALDG.2D" in sass and "UTMALDG.3D" in sass
     assert "DADD" in sass and "DMUL" in sass
+
+
+def test_missing_library_fails_loudly(tmp_path, monkeypatch):
+    """No CPU fallback: without libsrj.so the operator layer raises."""
+    from paper_2011_06636_b200 import _lib
+    monkeypatch.setattr(_lib, "_lib", None)
+    with pytest.raises(_lib.SrjLibraryError, match="no CPU fallback"):
+        _lib.load(str(tmp_path / "libsrj.so"))
