@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define SRJ_ABI_VERSION 1
+#define SRJ_ABI_VERSION 2
 
 enum srj_status {
     SRJ_OK = 0,
@@ -66,7 +66,9 @@ enum srj_family {
     SRJ_STENCIL_2D5 = 2,     /* 2D 5-point, (-1,-1, 4,-1,-1)*dx2            */
     SRJ_STENCIL_3D7 = 3,     /* 3D 7-point, 6*dx2 diagonal, -dx2 neighbours  */
     SRJ_STENCIL_2D5_VAR = 4, /* 2D 5-point, harmonic-mean face coefficients  */
-    SRJ_CSR = 5              /* general canonical CSR matrix (sparse.SparseMatrix) */
+    SRJ_CSR = 5,             /* general canonical CSR matrix (sparse.SparseMatrix) */
+    SRJ_STENCIL_3D7_VAR = 6, /* 3D 7-point, harmonic-mean face coefficients  */
+    SRJ_STENCIL_1D3_VAR = 7  /* 1D 3-point, face coefficients                */
 };
 
 /* Outcome of one cycle; mirrors the reference's CycleStats plus the buffer
@@ -85,8 +87,13 @@ typedef struct srj_op_desc {
     int64_t nx, ny, nz;    /* interior extents of THIS operator's grid (slab); unused axes = 1 */
     double  dx2;           /* constant coefficient scale (N+1)^2 (ignored for *_VAR) */
     /* *_VAR only: face coefficients already scaled by dx2, device pointers.
-     * face_x: ny rows of nx+1 faces (face i sits between points i-1 and i);
-     * face_y: ny+1 rows of nx faces (row j sits between rows j-1 and j). */
+     * Off-diagonals are -face; the diagonal is the sum of the point's faces in
+     * the order west, east (, south, north (, bottom, top)).
+     * face_x: ny*nz rows of nx+1 faces (face i sits between points i-1 and i);
+     * face_y: nz planes of ny+1 rows of nx faces (row j sits between rows j-1
+     *         and j); unused in 1D;
+     * face_z (3D, at the end of the struct): nz+1 planes of ny x nx faces
+     *         (plane z sits between planes z-1 and z). */
     const double* face_x;
     const double* face_y;
     /* SRJ_CSR only (nx = n, ny = nz = 1; vectors carry no ghosts): canonical
@@ -97,6 +104,8 @@ typedef struct srj_op_desc {
     const int32_t* col_idx;
     const double* values;
     const double* inv_diag;
+    /* SRJ_STENCIL_3D7_VAR only (ABI 2) */
+    const double* face_z;
 } srj_op_desc;
 
 typedef struct srj_cycle_out {
@@ -141,7 +150,7 @@ enum srj_cycle_kernel {
     SRJ_KERNEL_TB2D = 1,       /* temporally blocked 2D (sweeps_per_pass > 1)   */
     SRJ_KERNEL_TILE2D = 2,     /* TMA tile streaming 2D (constant / variable)   */
     SRJ_KERNEL_PLANE3D = 3,    /* TMA plane streaming 3D                        */
-    SRJ_KERNEL_WS2D = 4,       /* warp-streaming temporal blocking 2D           */
+    /* 4: retired (round-1 warp-streaming experiment, removed)                   */
     SRJ_KERNEL_TB3D = 5,       /* temporally blocked 3D z-wavefront (2 sweeps
                                   per pass when sweeps_per_pass > 1)            */
     SRJ_KERNEL_TBVAR = 6,      /* temporally blocked 2D variable coefficient    */
@@ -151,9 +160,8 @@ enum srj_cycle_kernel {
 
 /* Temporally blocked 2D kernel used when sweeps_per_pass > 1. */
 enum srj_tb_kind {
-    SRJ_TB_TILE = 0,           /* TMA-staged overlapped tiles (srj_tb.cu), default */
-    SRJ_TB_WARP_STREAM = 1     /* barrier-free warp streaming (srj_ws2d.cu),
-                                  experimental, <= 4 sweeps per pass              */
+    SRJ_TB_TILE = 0            /* TMA-staged overlapped tiles (srj_tb.cu), the only
+                                  kind; other values return SRJ_BAD_ARGUMENT     */
 };
 int srj_op_set_temporal_kernel(srj_op* op, int32_t kind);
 int srj_op_describe(const srj_op* op, srj_op_info* info);

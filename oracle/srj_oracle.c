@@ -18,7 +18,13 @@
  *
  * Vectors are plain n-arrays (no ghosts).  Families: 1 = 1D 3-pt, 2 = 2D 5-pt,
  * 3 = 3D 7-pt (constant coefficient, off = -dx2, diag = 2d*dx2), 4 = 2D 5-pt
- * variable coefficient with faces fx (ny x (nx+1)) and fy ((ny+1) x nx).
+ * variable coefficient with faces fx (ny x (nx+1)) and fy ((ny+1) x nx),
+ * 6 = 3D 7-pt variable coefficient with faces fx (nz*ny rows of nx+1), fy (nz
+ * planes of (ny+1) x nx) and fz ((nz+1) planes of ny x nx), 7 = 1D 3-pt
+ * variable coefficient with faces fx (nx+1).  Variable-coefficient operators
+ * are symmetric with off-diagonals -face and the diagonal the sum of the
+ * point's faces in the order west, east, south, north, bottom, top (the CSR
+ * the golden scripts hand the reference via SparseMatrix.from_coo).
  */
 #include <math.h>
 #include <stdint.h>
@@ -34,7 +40,21 @@ typedef struct {
     double dx2;
     const double* fx;
     const double* fy;
+    const double* fz;
 } oracle_op;
+
+/* 3D variable coefficient: faces of point (i, j, z). */
+static inline void faces3(const oracle_op* op, int64_t i, int64_t j, int64_t z, double* cw,
+                          double* ce, double* cs, double* cn, double* cb, double* ct) {
+    const int64_t nx = op->nx, ny = op->ny;
+    const double* fxr = op->fx + (z * ny + j) * (nx + 1);
+    *cw = fxr[i];
+    *ce = fxr[i + 1];
+    *cs = op->fy[(z * (ny + 1) + j) * nx + i];
+    *cn = op->fy[(z * (ny + 1) + j + 1) * nx + i];
+    *cb = op->fz[(z * ny + j) * nx + i];
+    *ct = op->fz[((z + 1) * ny + j) * nx + i];
+}
 
 static inline double diag_var(const oracle_op* op, int64_t i, int64_t j) {
     const double* fxr = op->fx + j * (op->nx + 1);
@@ -69,6 +89,22 @@ static inline double row_apply(const oracle_op* op, const double* x, int64_t k,
         if (i < nx - 1) y += c * x[k + 1];
         if (j < ny - 1) y += c * x[k + nx];
         if (z < nz - 1) y += c * x[k + pl];
+    } else if (op->fam == 6) {
+        double cw, ce, cs, cn, cb, ct;
+        faces3(op, i, j, z, &cw, &ce, &cs, &cn, &cb, &ct);
+        const double d = ((((cw + ce) + cs) + cn) + cb) + ct;
+        if (z > 0) y += (-cb) * x[k - pl];
+        if (j > 0) y += (-cs) * x[k - nx];
+        if (i > 0) y += (-cw) * x[k - 1];
+        y += d * x[k];
+        if (i < nx - 1) y += (-ce) * x[k + 1];
+        if (j < ny - 1) y += (-cn) * x[k + nx];
+        if (z < nz - 1) y += (-ct) * x[k + pl];
+    } else if (op->fam == 7) {
+        const double cw = op->fx[i], ce = op->fx[i + 1];
+        if (i > 0) y += (-cw) * x[k - 1];
+        y += (cw + ce) * x[k];
+        if (i < nx - 1) y += (-ce) * x[k + 1];
     } else {
         const double* fxr = op->fx + j * (nx + 1);
         if (j > 0) y += (-op->fy[j * nx + i]) * x[k - nx];
@@ -80,10 +116,16 @@ static inline double row_apply(const oracle_op* op, const double* x, int64_t k,
     return y;
 }
 
-static inline double inv_diag_at(const oracle_op* op, int64_t i, int64_t j) {
+static inline double inv_diag_at(const oracle_op* op, int64_t i, int64_t j, int64_t z) {
     double d;
     if (op->fam == 4) {
         d = diag_var(op, i, j);
+    } else if (op->fam == 6) {
+        double cw, ce, cs, cn, cb, ct;
+        faces3(op, i, j, z, &cw, &ce, &cs, &cn, &cb, &ct);
+        d = ((((cw + ce) + cs) + cn) + cb) + ct;
+    } else if (op->fam == 7) {
+        d = op->fx[i] + op->fx[i + 1];
     } else {
         d = (op->fam == 1 ? 2.0 : op->fam == 2 ? 4.0 : 6.0) * op->dx2;
     }
@@ -92,9 +134,9 @@ static inline double inv_diag_at(const oracle_op* op, int64_t i, int64_t j) {
 
 /* r = b - A x over all points; returns sum r^2 (sequential per thread chunk). */
 double oracle_residual(int fam, int64_t nx, int64_t ny, int64_t nz, double dx2,
-                       const double* fx, const double* fy, const double* x,
+                       const double* fx, const double* fy, const double* fz, const double* x,
                        const double* b, double* r_out) {
-    const oracle_op op = {fam, nx, ny, nz, dx2, fx, fy};
+    const oracle_op op = {fam, nx, ny, nz, dx2, fx, fy, fz};
     const int64_t rows = ny * nz;
     double total = 0.0;
 #pragma omp parallel for schedule(static) reduction(+ : total)
@@ -114,16 +156,16 @@ double oracle_residual(int fam, int64_t nx, int64_t ny, int64_t nz, double dx2,
 
 /* x_out = x + w*(inv_diag*r)  (solver.py:231). */
 void oracle_update(int fam, int64_t nx, int64_t ny, int64_t nz, double dx2,
-                   const double* fx, const double* fy, const double* x, const double* r,
-                   double w, double* x_out) {
-    const oracle_op op = {fam, nx, ny, nz, dx2, fx, fy};
+                   const double* fx, const double* fy, const double* fz, const double* x,
+                   const double* r, double w, double* x_out) {
+    const oracle_op op = {fam, nx, ny, nz, dx2, fx, fy, fz};
     const int64_t rows = ny * nz;
 #pragma omp parallel for schedule(static)
     for (int64_t row = 0; row < rows; ++row) {
-        const int64_t j = row % ny;
+        const int64_t j = row % ny, z = row / ny;
         for (int64_t i = 0; i < nx; ++i) {
             const int64_t k = row * nx + i;
-            const double t = inv_diag_at(&op, i, j) * r[k];
+            const double t = inv_diag_at(&op, i, j, z) * r[k];
             x_out[k] = x[k] + w * t;
         }
     }
@@ -131,8 +173,9 @@ void oracle_update(int fam, int64_t nx, int64_t ny, int64_t nz, double dx2,
 
 /* y = A x. */
 void oracle_matvec(int fam, int64_t nx, int64_t ny, int64_t nz, double dx2,
-                   const double* fx, const double* fy, const double* x, double* y) {
-    const oracle_op op = {fam, nx, ny, nz, dx2, fx, fy};
+                   const double* fx, const double* fy, const double* fz, const double* x,
+                   double* y) {
+    const oracle_op op = {fam, nx, ny, nz, dx2, fx, fy, fz};
     const int64_t rows = ny * nz;
 #pragma omp parallel for schedule(static)
     for (int64_t row = 0; row < rows; ++row) {

@@ -145,11 +145,11 @@ def clib():
         i64 = ctypes.c_int64
         L.oracle_residual.restype = ctypes.c_double
         L.oracle_residual.argtypes = [ctypes.c_int, i64, i64, i64, ctypes.c_double,
-                                      dp, dp, dp, dp, dp]
+                                      dp, dp, dp, dp, dp, dp]
         L.oracle_update.argtypes = [ctypes.c_int, i64, i64, i64, ctypes.c_double,
-                                    dp, dp, dp, dp, ctypes.c_double, dp]
+                                    dp, dp, dp, dp, dp, ctypes.c_double, dp]
         L.oracle_matvec.argtypes = [ctypes.c_int, i64, i64, i64, ctypes.c_double,
-                                    dp, dp, dp, dp]
+                                    dp, dp, dp, dp, dp]
         L.oracle_threads.restype = ctypes.c_int
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         _lib = L
@@ -162,7 +162,7 @@ def _p(a):
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
 
 
-FAMILY_CODE = {"1d3": 1, "2d5": 2, "3d7": 3, "2d5var": 4}
+FAMILY_CODE = {"1d3": 1, "2d5": 2, "3d7": 3, "2d5var": 4, "3d7var": 6, "1d3var": 7}
 
 
 @dataclass
@@ -176,6 +176,7 @@ class StencilCPU:
     dx2: float = 0.0
     fx: np.ndarray | None = None
     fy: np.ndarray | None = None
+    fz: np.ndarray | None = None
 
     @property
     def n(self):
@@ -183,7 +184,7 @@ class StencilCPU:
 
     def _args(self):
         return (FAMILY_CODE[self.family], self.nx, self.ny, self.nz, float(self.dx2),
-                _p(self.fx), _p(self.fy))
+                _p(self.fx), _p(self.fy), _p(self.fz))
 
     def residual(self, x, b):
         r = np.empty(self.n)
@@ -221,14 +222,17 @@ class CsrCPU:
         return self.csr.dot(x)
 
 
-def stencil(family, n, dx2=None, fx=None, fy=None):
-    dims = {"1d3": (n, 1, 1), "2d5": (n, n, 1), "3d7": (n, n, n), "2d5var": (n, n, 1)}[family]
+def stencil(family, n, dx2=None, fx=None, fy=None, fz=None, dims=None):
+    if dims is None:
+        dims = {"1d3": (n, 1, 1), "2d5": (n, n, 1), "3d7": (n, n, n), "2d5var": (n, n, 1),
+                "3d7var": (n, n, n), "1d3var": (n, 1, 1)}[family]
+    dims = tuple(dims) + (1,) * (3 - len(dims))
     if dx2 is None:
-        dx2 = (n + 1.0) ** 2
-    if fx is not None:
-        fx = np.ascontiguousarray(fx, dtype=np.float64)
-        fy = np.ascontiguousarray(fy, dtype=np.float64)
-    return StencilCPU(family, *dims, dx2=dx2, fx=fx, fy=fy)
+        dx2 = (dims[0] + 1.0) ** 2
+
+    def arr(a):
+        return None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+    return StencilCPU(family, *dims, dx2=dx2, fx=arr(fx), fy=arr(fy), fz=arr(fz))
 
 
 # ---------------------------------------------------------------- solver

@@ -13,7 +13,8 @@ from .chebyshev import amplification_eval, cheb_eval, cheb_roots, lambda_max, la
 from .operators import (DeviceOperator, Field, StencilOperator, fill_uniform_rhs,
                         relative_residual)
 from .problems import (ABSOLUTE_L2, CONFIGS, RELATIVE_L2, SOLUTION_DIFF_INF, ProblemInstance,
-                       baseline_problem, config_problem, diffusion_2d_varcoef,
+                       baseline_problem, config_problem, diffusion_1d_varcoef,
+                       diffusion_2d_varcoef, diffusion_3d_varcoef,
                        laplace_2d_neumann, poisson_1d, poisson_2d, poisson_3d,
                        random_tridiagonal)
 from .sparse import (SparseMatrix, diff_inf, matvec, relative_residual_l2, residual_l2,

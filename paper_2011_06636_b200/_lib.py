@@ -14,10 +14,11 @@ from ctypes import POINTER, c_double, c_int32, c_int64, c_uint64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsrj.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 SRJ_OK, SRJ_DIVERGED, SRJ_BAD_ARGUMENT, SRJ_CUDA_ERROR = 0, 1, 2, 3
 SRJ_STENCIL_1D3, SRJ_STENCIL_2D5, SRJ_STENCIL_3D7, SRJ_STENCIL_2D5_VAR, SRJ_CSR = 1, 2, 3, 4, 5
+SRJ_STENCIL_3D7_VAR, SRJ_STENCIL_1D3_VAR = 6, 7
 CYCLE_RAN, CYCLE_CONVERGED, CYCLE_DIVERGED = 0, 1, 2
 
 # Every symbol include/srj.h declares (checked by tests/test_abi.py).
@@ -32,7 +33,7 @@ EXPORTED_SYMBOLS = (
 )
 SOLVE_PAUSED, SOLVE_CONVERGED, SOLVE_DIVERGED, SOLVE_BUDGET = 0, 1, 2, 3
 SOLVE_HEURISTIC, SOLVE_INCREASING, SOLVE_FIXED = 0, 1, 2
-TB_TILE, TB_WARP_STREAM = 0, 1
+TB_TILE = 0
 
 
 class BatchJob(ctypes.Structure):
@@ -48,6 +49,7 @@ class OpDesc(ctypes.Structure):
         ("face_x", c_void_p), ("face_y", c_void_p),
         ("nnz", c_int64), ("row_ptr", c_void_p), ("col_idx", c_void_p),
         ("values", c_void_p), ("inv_diag", c_void_p),
+        ("face_z", c_void_p),
     ]
 
 
@@ -87,7 +89,6 @@ class OpInfo(ctypes.Structure):
                1: "srj::k_tb2d_cycle (TMA temporal blocking)",
                2: "srj::k_cycle2d (TMA tile streaming)",
                3: "srj::k_cycle3d (TMA plane ring)",
-               4: "srj::k_ws2d_cycle (warp-streaming temporal blocking)",
                5: "srj::k_tb3d_cycle (TMA z-wavefront temporal blocking)",
                6: "srj::k_tbvar_cycle (TMA var-coef temporal blocking)",
                7: "srj::k_small_cycle_1d (single-CTA shared-memory cycle)",
@@ -141,11 +142,18 @@ def _declare(L):
     L.srj_op_planes.restype = c_int64
 
 
-def load(path: str = LIB_PATH):
-    """Load and type the shared library (no CUDA call is made)."""
+STRESS_LIB_PATH = os.path.join(_HERE, "libsrj_stress.so")
+
+
+def load(path: str | None = None):
+    """Load and type the shared library (no CUDA call is made).  SRJ_LIBRARY
+    selects another build of the same ABI (tests: the race/bounds stress
+    build libsrj_stress.so, csrc/srj_stress.cuh)."""
     global _lib
     if _lib is not None:
         return _lib
+    if path is None:
+        path = os.environ.get("SRJ_LIBRARY") or LIB_PATH
     if not os.path.exists(path):
         raise SrjLibraryError(
             f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"

@@ -27,7 +27,6 @@
 #include "srj_stencil.cuh"
 #include "srj_2d.cuh"
 #include "srj_3d.cuh"
-#include "srj_ws2d.cuh"
 #include "srj_tb.cuh"
 #include "srj_walk.cuh"
 
@@ -603,8 +602,6 @@ struct srj_op {
     TbvPlan tbv;                 // var-coef 2D temporal-blocking plan (srj_tbvar.cu)
     Plan3D p3;                   // plane-streaming 3D plan (srj_3d.cuh)
     Plan2D p2;                   // tile-streaming 2D plan (srj_2d.cuh)
-    WsPlan ws;                   // warp-streaming temporal blocking (srj_ws2d.cuh)
-    int tb_kind = SRJ_TB_TILE;   // measured faster on B200
     // srj_sweep_planes scratch, one set per slot (concurrent launches)
     double* slot_part[kSlots] = {nullptr, nullptr};
     unsigned* slot_counter = nullptr;  // device [kSlots], zero between launches
@@ -625,6 +622,8 @@ static const void* cycle_kernel_for(int fam) {
         case F2D: return cycle_kernel<F2D>();
         case F3D: return cycle_kernel<F3D>();
         case FCSR: return cycle_kernel<FCSR>();
+        case F3DV: return cycle_kernel<F3DV>();
+        case F1DV: return cycle_kernel<F1DV>();
         default: return cycle_kernel<F2DV>();
     }
 }
@@ -638,6 +637,8 @@ static int launch_apply(srj_op* op, const double* x, double* out, const double* 
         case F2D: k_apply<F2D, MODE><<<blocks, kThreads, 0, st>>>(op->g, x, out, b, w); break;
         case F3D: k_apply<F3D, MODE><<<blocks, kThreads, 0, st>>>(op->g, x, out, b, w); break;
         case FCSR: k_apply<FCSR, MODE><<<blocks, kThreads, 0, st>>>(op->g, x, out, b, w); break;
+        case F3DV: k_apply<F3DV, MODE><<<blocks, kThreads, 0, st>>>(op->g, x, out, b, w); break;
+        case F1DV: k_apply<F1DV, MODE><<<blocks, kThreads, 0, st>>>(op->g, x, out, b, w); break;
         default: k_apply<F2DV, MODE><<<blocks, kThreads, 0, st>>>(op->g, x, out, b, w); break;
     }
     CUDA_TRY(cudaGetLastError());
@@ -653,22 +654,26 @@ const char* srj_last_error(void) { return g_last_error.c_str(); }
 int srj_op_create(const srj_op_desc* d, srj_op** out) {
     if (!d || !out) return fail(SRJ_BAD_ARGUMENT, "null argument");
     *out = nullptr;
-    if (d->family < SRJ_STENCIL_1D3 || d->family > SRJ_CSR)
+    if (d->family < SRJ_STENCIL_1D3 || d->family > SRJ_STENCIL_1D3_VAR)
         return fail(SRJ_BAD_ARGUMENT, "unknown stencil family");
     if (d->nx < 1 || d->ny < 1 || d->nz < 1)
         return fail(SRJ_BAD_ARGUMENT, "extents must be positive");
-    const bool var = d->family == SRJ_STENCIL_2D5_VAR;
+    const bool var = d->family == SRJ_STENCIL_2D5_VAR || d->family == SRJ_STENCIL_3D7_VAR ||
+                     d->family == SRJ_STENCIL_1D3_VAR;
     const bool csr = d->family == SRJ_CSR;
-    if (var && (!d->face_x || !d->face_y))
-        return fail(SRJ_BAD_ARGUMENT, "variable-coefficient operator needs face_x and face_y");
+    const bool is1d = d->family == SRJ_STENCIL_1D3 || d->family == SRJ_STENCIL_1D3_VAR;
+    const bool is3d = d->family == SRJ_STENCIL_3D7 || d->family == SRJ_STENCIL_3D7_VAR;
+    if (var && (!d->face_x || (!is1d && !d->face_y) || (is3d && !d->face_z)))
+        return fail(SRJ_BAD_ARGUMENT,
+                    "variable-coefficient operator needs face_x (and face_y in 2D/3D, face_z in 3D)");
     if (csr && (!d->row_ptr || !d->col_idx || !d->values || !d->inv_diag || d->ny != 1 ||
                 d->nz != 1 || d->nnz < 1))
         return fail(SRJ_BAD_ARGUMENT, "CSR operator needs row_ptr, col_idx, values, inv_diag, nnz and ny == nz == 1");
     if (!var && !csr && !(d->dx2 > 0.0))
         return fail(SRJ_BAD_ARGUMENT, "dx2 must be positive");
-    if (d->family == SRJ_STENCIL_1D3 && (d->ny != 1 || d->nz != 1))
+    if (is1d && (d->ny != 1 || d->nz != 1))
         return fail(SRJ_BAD_ARGUMENT, "1D operator needs ny == nz == 1");
-    if ((d->family == SRJ_STENCIL_2D5 || var) && d->nz != 1)
+    if ((d->family == SRJ_STENCIL_2D5 || d->family == SRJ_STENCIL_2D5_VAR) && d->nz != 1)
         return fail(SRJ_BAD_ARGUMENT, "2D operator needs nz == 1");
     const long long rows = d->ny * d->nz;
     const long long upr = (d->nx + 31) / 32;
@@ -685,18 +690,17 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
     g.ny = (int)d->ny;
     g.nz = (int)d->nz;
     g.n = d->nx * d->ny * d->nz;
-    g.plane = csr ? 0
-                  : d->family == SRJ_STENCIL_1D3 ? 1
-                  : (d->family == SRJ_STENCIL_3D7 ? d->nx * d->ny : d->nx);
+    g.plane = csr ? 0 : is1d ? 1 : (is3d ? d->nx * d->ny : d->nx);
     g.rows = (int)rows;
     g.upr = (int)upr;
     g.units = (int)(rows * upr);
-    const double dim = d->family == SRJ_STENCIL_1D3 ? 1.0 : (d->family == SRJ_STENCIL_3D7 ? 3.0 : 2.0);
+    const double dim = is1d ? 1.0 : (is3d ? 3.0 : 2.0);
     g.c_off = -1.0 * d->dx2;                  // reference problems.py:59,170
     g.c_diag = (2.0 * dim) * d->dx2;          // 2*dx2, 4*dx2, 6*dx2 (problems.py:58,164)
     g.inv_diag = 1.0 / g.c_diag;              // sparse.py:44
     g.fx = d->face_x;
     g.fy = d->face_y;
+    g.fz = is3d && var ? d->face_z : nullptr;
     g.rp = reinterpret_cast<const long long*>(d->row_ptr);
     g.ci = d->col_idx;
     g.cv = d->values;
@@ -735,11 +739,6 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("allocation failed: ") + cudaGetErrorString(e));
     }
-    if ((e = ws_plan_init(op->ws, g, op->num_sms)) != cudaSuccess) {
-        srj_op_destroy(op);
-        return fail(SRJ_CUDA_ERROR, std::string("warp-stream plan setup failed: ") + cudaGetErrorString(e));
-    }
-    if (const char* kind = getenv("SRJ_TB_KIND")) op->tb_kind = atoi(kind);
     if ((e = plan2d_init(op->p2, g, op->num_sms)) != cudaSuccess) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("2D plan setup failed: ") + cudaGetErrorString(e));
@@ -772,7 +771,6 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
     // vs 603 for the HBM-bound plane ring), else one per pass.
     op->sweeps_per_pass = (op->tb.supported || op->tbv.supported) ? 6
                           : op->tb3.supported                     ? 2
-                          : op->ws.supported                      ? 4
                                                                   : 1;
     op->slot_capacity = std::max(op->p3.slots, kApplyBlocksPerSm * op->num_sms);
     for (int s = 0; s < kSlots; ++s) {
@@ -819,7 +817,7 @@ int srj_op_layout(const srj_op* op, int64_t* n, int64_t* halo) {
 
 int srj_op_diag(const srj_op* op, double* diag, double* inv_diag) {
     if (!op) return fail(SRJ_BAD_ARGUMENT, "null operator");
-    if (op->g.fam == F2DV || op->g.fam == FCSR)
+    if (op->g.fam == F2DV || op->g.fam == F3DV || op->g.fam == F1DV || op->g.fam == FCSR)
         return fail(SRJ_BAD_ARGUMENT, "this operator's diagonal is per point");
     if (diag) *diag = op->g.c_diag;
     if (inv_diag) *inv_diag = op->g.inv_diag;
@@ -828,9 +826,10 @@ int srj_op_diag(const srj_op* op, double* diag, double* inv_diag) {
 
 int srj_op_set_temporal_kernel(srj_op* op, int32_t kind) {
     if (!op) return fail(SRJ_BAD_ARGUMENT, "null operator");
-    if (kind != SRJ_TB_TILE && kind != SRJ_TB_WARP_STREAM)
-        return fail(SRJ_BAD_ARGUMENT, "unknown temporal-blocking kernel");
-    op->tb_kind = kind;
+    // The warp-streaming variant (round 1: 196 vs 555 GLUP/s) was removed; the
+    // tile kernel is the only 2D temporally blocked kernel.
+    if (kind != SRJ_TB_TILE)
+        return fail(SRJ_BAD_ARGUMENT, "unknown temporal-blocking kernel (only SRJ_TB_TILE)");
     return SRJ_OK;
 }
 
@@ -850,8 +849,6 @@ int srj_op_describe(const srj_op* op, srj_op_info* info) {
     info->cycle_kernel = (op->sweeps_per_pass > 1 && op->tbv.supported)  ? SRJ_KERNEL_TBVAR
                          : (op->sweeps_per_pass > 1 && op->tb3.supported) ? SRJ_KERNEL_TB3D
                          : op->p3.supported                               ? SRJ_KERNEL_PLANE3D
-                         : (op->sweeps_per_pass > 1 && op->ws.supported &&
-                            op->tb_kind == SRJ_TB_WARP_STREAM) ? SRJ_KERNEL_WS2D
                          : (op->sweeps_per_pass > 1 && op->tb.supported) ? SRJ_KERNEL_TB2D
                          : op->p2.supported                               ? SRJ_KERNEL_TILE2D
                          : reg1d_ok(op->g) ? SRJ_KERNEL_REG1D
@@ -960,11 +957,6 @@ int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
         CUDA_TRY(launch3d_cycle(op->p3, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,
                                 op->partials, op->hist, op->out_i, op->out_d, st));
         out->launches = 1;
-    } else if (op->sweeps_per_pass > 1 && op->ws.supported && op->tb_kind == SRJ_TB_WARP_STREAM) {
-        CUDA_TRY(ws_launch_cycle(op->ws, op->g, x, x_alt, b, omegas_dev, Meff,
-                                 op->sweeps_per_pass, tol, baseline, op->partials, op->hist,
-                                 op->out_i, op->out_d, st));
-        out->launches = 1;
     } else if (op->sweeps_per_pass > 1 && op->tb.supported) {
         CUDA_TRY(tb_launch_cycle(op->tb, op->g, x, x_alt, b, omegas_dev, Meff,
                                  op->sweeps_per_pass, tol, baseline, op->partials, op->hist,
@@ -1003,7 +995,6 @@ static int solve_kernel(const srj_op* op) {
     if (op->sweeps_per_pass <= 1) return 0;
     if (op->tbv.supported) return SRJ_KERNEL_TBVAR;
     if (op->tb3.supported) return SRJ_KERNEL_TB3D;
-    if (op->tb_kind == SRJ_TB_WARP_STREAM && op->ws.supported) return 0;
     if (op->tb.supported) return SRJ_KERNEL_TB2D;
     return 0;
 }
@@ -1195,7 +1186,8 @@ int srj_matvec(srj_op* op, const double* x, double* y, void* stream) {
 
 int64_t srj_op_planes(const srj_op* op) {
     if (!op) return -1;
-    return op->g.fam == F3D ? op->g.nz : ((op->g.fam == F1D || op->g.fam == FCSR) ? 1 : op->g.ny);
+    return (op->g.fam == F3D || op->g.fam == F3DV) ? op->g.nz
+           : ((op->g.fam == F1D || op->g.fam == F1DV || op->g.fam == FCSR) ? 1 : op->g.ny);
 }
 
 int srj_sweep_planes(srj_op* op, const double* x, double* x_out, const double* b, double omega,
@@ -1219,10 +1211,11 @@ int srj_sweep_planes(srj_op* op, const double* x, double* x_out, const double* b
                                 op->slot_part[slot], op->slot_counter + slot, partial_dev, st));
         return SRJ_OK;
     }
-    const long long rows_per_plane = g.fam == F3D ? g.ny : (g.fam == F1D ? 1 : 1);
-    const long long per_plane = (g.fam == F1D ? 1 : rows_per_plane) * g.upr;
-    const int ub = (int)(z_begin * (g.fam == F1D ? g.units : per_plane));
-    const int ue = (int)(z_end * (g.fam == F1D ? g.units : per_plane));
+    const bool is1d = g.fam == F1D || g.fam == F1DV || g.fam == FCSR;
+    const long long rows_per_plane = (g.fam == F3D || g.fam == F3DV) ? g.ny : 1;
+    const long long per_plane = rows_per_plane * g.upr;
+    const int ub = (int)(z_begin * (is1d ? g.units : per_plane));
+    const int ue = (int)(z_end * (is1d ? g.units : per_plane));
     const int blocks = (int)std::max<long long>(
         1, std::min<long long>((ue - ub + 7) / 8, (long long)kApplyBlocksPerSm * op->num_sms));
     double* bp = op->slot_part[slot];
@@ -1239,6 +1232,8 @@ int srj_sweep_planes(srj_op* op, const double* x, double* x_out, const double* b
         case F2D: SRJ_RANGE(F2D) break;
         case F3D: SRJ_RANGE(F3D) break;
         case FCSR: SRJ_RANGE(FCSR) break;
+        case F3DV: SRJ_RANGE(F3DV) break;
+        case F1DV: SRJ_RANGE(F1DV) break;
         default: SRJ_RANGE(F2DV) break;
     }
 #undef SRJ_RANGE

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "srj_stress.cuh"
+
 // Separately rounded fp64 operations: the reference's scipy csr_matvec and
 // numpy ufuncs round every multiply and add on their own, so the device must
 // never contract them into FMAs (bit-identical iterates, SURVEY §8a parity
@@ -14,7 +16,7 @@
 
 namespace srj {
 
-enum Family { F1D = 1, F2D = 2, F3D = 3, F2DV = 4, FCSR = 5 };
+enum Family { F1D = 1, F2D = 2, F3D = 3, F2DV = 4, FCSR = 5, F3DV = 6, F1DV = 7 };
 
 // Cycle outcome codes (match enum srj_cycle_status in include/srj.h).
 constexpr int kStatusRan = 0;
@@ -62,6 +64,7 @@ struct Geom {
     double inv_diag;    // 1.0 / c_diag
     const double* fx;   // var-coef faces (see srj.h)
     const double* fy;
+    const double* fz;
     // general CSR operator (canonical: sorted columns, no duplicates)
     const long long* rp;  // row pointers [n+1]
     const int* ci;        // column indices [nnz]

@@ -64,6 +64,39 @@ __device__ __forceinline__ double apply_at(const Geom& g, const double* x,
         for (long long jj = g.rp[k]; jj < e; ++jj) y = DADD(y, DMUL(__ldg(g.cv + jj), x[__ldg(g.ci + jj)]));
         xc = x[k];
         inv = __ldg(g.cinv + k);
+    } else if constexpr (FAM == F3DV) {
+        // faces pre-scaled by dx2; diagonal = sum of the point's faces in the
+        // order west, east, south, north, bottom, top; j is the x-row index
+        // z*ny + jy (the walker's row)
+        const long long nx = g.nx, pl = g.plane;
+        const int z = j / g.ny, jy = j - z * g.ny;
+        const double* fxr = g.fx + (long long)j * (nx + 1);
+        const double cw = __ldg(fxr + i), ce = __ldg(fxr + i + 1);
+        const double* fyp = g.fy + (long long)(j + z) * nx + i;  // row z*(ny+1) + jy
+        const double cs = __ldg(fyp), cn = __ldg(fyp + nx);
+        const double cb = __ldg(g.fz + k), ct = __ldg(g.fz + k + pl);
+        const double diag = DADD(DADD(DADD(DADD(DADD(cw, ce), cs), cn), cb), ct);
+        inv = __ddiv_rn(1.0, diag);
+        xc = x[k];
+        const double xs = jy > 0 ? x[k - nx] : 0.0;
+        const double xn = jy < g.ny - 1 ? x[k + nx] : 0.0;
+        const double xw = i > 0 ? x[k - 1] : 0.0;
+        const double xe = i < g.nx - 1 ? x[k + 1] : 0.0;
+        y = DADD(0.0, DMUL(-cb, x[k - pl]));
+        y = DADD(y, DMUL(-cs, xs));
+        y = DADD(y, DMUL(-cw, xw));
+        y = DADD(y, DMUL(diag, xc));
+        y = DADD(y, DMUL(-ce, xe));
+        y = DADD(y, DMUL(-cn, xn));
+        y = DADD(y, DMUL(-ct, x[k + pl]));
+    } else if constexpr (FAM == F1DV) {
+        const double cw = __ldg(g.fx + k), ce = __ldg(g.fx + k + 1);
+        const double diag = DADD(cw, ce);
+        inv = __ddiv_rn(1.0, diag);
+        xc = x[k];
+        y = DADD(0.0, DMUL(-cw, x[k - 1]));
+        y = DADD(y, DMUL(diag, xc));
+        y = DADD(y, DMUL(-ce, x[k + 1]));
     } else {  // F2DV: faces pre-scaled by dx2; CSR stores -face off the diagonal
         const long long nx = g.nx;
         const long long row = j;

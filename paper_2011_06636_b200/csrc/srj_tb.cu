@@ -145,6 +145,7 @@ struct TbLayout {
 // CW contiguous doubles at a 16-byte aligned shared address.
 template <int CW>
 __device__ __forceinline__ void lds_cols(double (&d)[CW], const double* p) {
+    SRJ_ASSERT_SMEM(p, CW * sizeof(double), tb_smem);
 #pragma unroll
     for (int j = 0; j < CW; j += 2) {
         const double2 v = *reinterpret_cast<const double2*>(p + j);
@@ -154,6 +155,7 @@ __device__ __forceinline__ void lds_cols(double (&d)[CW], const double* p) {
 }
 template <int CW>
 __device__ __forceinline__ void sts_cols(double* p, const double (&d)[CW]) {
+    SRJ_ASSERT_SMEM(p, CW * sizeof(double), tb_smem);
 #pragma unroll
     for (int j = 0; j < CW; j += 2) *reinterpret_cast<double2*>(p + j) = make_double2(d[j], d[j + 1]);
 }
@@ -178,6 +180,13 @@ __device__ __forceinline__ void fma_sq_if(double& acc, double r, unsigned cond) 
         : "+d"(acc)
         : "d"(r), "r"(cond));
 }
+
+#ifdef SRJ_STRESS
+// Negative control of the stress build: SRJ_STRESS_BREAK=1 in the environment
+// skips the halo hand-off wait, a deliberate race the stress parity tests must
+// catch (tests/test_gpu_stress.py).
+__device__ int tb_stress_break = 0;
+#endif
 
 template <int K>
 struct TileRegs {
@@ -284,7 +293,10 @@ __device__ __forceinline__ void tile_sweeps(TileRegs<K>& R, const double* omegas
         static_assert(V == 6, "interior rows 1..4 form one group");
         group(1, 2, 3, 4);
         {  // halos of sub-sweep t were published by every warp (t = 0: at tile start)
-            mbar_wait(L::hbar(na & 1), (na >> 1) & 1);
+#ifdef SRJ_STRESS
+            if (!tb_stress_break)
+#endif
+                mbar_wait(L::hbar(na & 1), (na >> 1) & 1);
             ++na;
         }
         lds_cols<CW>(hs, L::bot(hb + t) + warp * RX + col);        // bottom row of warp-1
@@ -414,8 +426,11 @@ __device__ __forceinline__ void tb2d_pass(const TbArgs& a, const CUtensorMap* tm
                 for (int j = 0; j < CW; j += 2) {
                     // a lane's column pair is owned / inside the grid as a whole
                     // (even nx, even ring and tile widths): one predicated store
-                    if ((storemask >> (v * CW + j)) & 1u)
+                    if ((storemask >> (v * CW + j)) & 1u) {
+                        SRJ_ASSERT(gy0 + v >= (SLAB ? a.row_lo : 0) && gy0 + v < (SLAB ? a.row_hi : ny) &&
+                                   gx0 + j >= 0 && gx0 + j + 1 < nx);
                         *reinterpret_cast<double2*>(row + j) = make_double2(R.x[v][j], R.x[v][j + 1]);
+                    }
                 }
             }
         }
@@ -527,6 +542,13 @@ cudaError_t tb_plan_init(TbPlan& plan, const Geom& g, int num_sms) {
     }
     plan.occupancy = std::min(occ[0], occ[1]);
     if (plan.occupancy < 1) return cudaSuccess;
+#ifdef SRJ_STRESS
+    {
+        const char* br = getenv("SRJ_STRESS_BREAK");
+        const int v = (br && atoi(br) == 1) ? 1 : 0;
+        if ((e = cudaMemcpyToSymbol(tb_stress_break, &v, sizeof(int))) != cudaSuccess) return e;
+    }
+#endif
     plan_tiles<0>(plan, g, num_sms);
     plan_tiles<1>(plan, g, num_sms);
     plan.supported = true;

@@ -95,6 +95,7 @@ __device__ __forceinline__ void fma_sq_if(double& acc, double r, bool cond) {
 }
 
 __device__ __forceinline__ void lds_pair(double (&d)[2], const double* p) {
+    SRJ_ASSERT_SMEM(p, 16, tb3_smem);
     const double2 v = *reinterpret_cast<const double2*>(p);
     d[0] = v.x;
     d[1] = v.y;

@@ -92,11 +92,13 @@ struct TbvLayout {
 };
 
 __device__ __forceinline__ void ld2(double (&d)[2], const double* p) {
+    SRJ_ASSERT_SMEM(p, 16, tbv_smem);
     const double2 v = *reinterpret_cast<const double2*>(p);
     d[0] = v.x;
     d[1] = v.y;
 }
 __device__ __forceinline__ void st2(double* p, const double (&d)[2]) {
+    SRJ_ASSERT_SMEM(p, 16, tbv_smem);
     *reinterpret_cast<double2*>(p) = make_double2(d[0], d[1]);
 }
 
@@ -324,8 +326,11 @@ __device__ __forceinline__ void tbv_pass(const TbvArgs& a, const CUtensorMap* tm
                 double* row = xout + (long long)(gy0 + v) * nx + gx0;
                 // a lane's column pair is owned / inside the grid as a whole
                 // (even nx, even ring and tile widths): one predicated store
-                if ((storemask >> (v * CW)) & 1u)
+                if ((storemask >> (v * CW)) & 1u) {
+                    SRJ_ASSERT(gy0 + v >= (SLAB ? a.row_lo : 0) && gy0 + v < (SLAB ? a.row_hi : ny) &&
+                               gx0 >= 0 && gx0 + 1 < nx);
                     *reinterpret_cast<double2*>(row) = make_double2(R.x[v][0], R.x[v][1]);
+                }
             }
         }
         // No barrier here: the halo parity runs on across tiles (hb) and the

@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "srj_stress.cuh"
+
 namespace srj {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -28,10 +30,28 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 
 // Plain arrival (count 1), no transaction bytes.
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    SRJ_JITTER(1);
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef SRJ_STRESS
+    // bounded wait: a lost arrival traps after ~2 s instead of hanging
+    const uint64_t t0 = stress_clock();
+    for (;;) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) break;
+        if (stress_clock() - t0 > 2000000000ull) __trap();
+    }
+    SRJ_JITTER(2);
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
@@ -39,11 +59,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+#endif
 }
 
 // 2D box load global -> shared, completion counted on `bar` in bytes.
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x0, int y0,
                                             uint64_t* bar) {
+    SRJ_JITTER(3);
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
@@ -54,6 +76,7 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 // 3D box load (x fastest, then y, then z planes).
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x0, int y0,
                                             int z0, uint64_t* bar) {
+    SRJ_JITTER(4);
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),

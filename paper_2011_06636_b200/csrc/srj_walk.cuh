@@ -51,6 +51,7 @@ __device__ __forceinline__ double walk_units(const Geom& g, const double* __rest
 }
 
 __device__ __forceinline__ void grid_barrier() {
+    SRJ_JITTER(5);
     if (gridDim.x == 1) {
         __syncthreads();
     } else {

@@ -32,6 +32,8 @@ FAMILIES = {
     "2d5": _lib.SRJ_STENCIL_2D5,
     "3d7": _lib.SRJ_STENCIL_3D7,
     "2d5var": _lib.SRJ_STENCIL_2D5_VAR,
+    "3d7var": _lib.SRJ_STENCIL_3D7_VAR,
+    "1d3var": _lib.SRJ_STENCIL_1D3_VAR,
 }
 
 
@@ -125,10 +127,12 @@ class DeviceOperator:
                    "srj_op_set_sweeps_per_pass")
 
     def set_temporal_kernel(self, kind: str) -> None:
-        """'tile' (default, TMA overlapped tiles) or 'warp_stream' (barrier-free,
-        experimental, at most 4 sweeps per pass): which temporally blocked 2D
-        kernel serves sweeps_per_pass > 1."""
-        code = {"tile": _lib.TB_TILE, "warp_stream": _lib.TB_WARP_STREAM}[kind]
+        """'tile' (TMA overlapped tiles): the temporally blocked 2D kernel that
+        serves sweeps_per_pass > 1 (the round-1 'warp_stream' experiment was
+        removed; any other kind raises ValueError)."""
+        if kind != "tile":
+            raise ValueError(f"unknown temporal kernel {kind!r} (only 'tile')")
+        code = _lib.TB_TILE
         _lib.check(_lib.lib().srj_op_set_temporal_kernel(self.handle, code),
                    "srj_op_set_temporal_kernel")
 
@@ -258,7 +262,26 @@ class Grid:
 
     @property
     def halo(self) -> int:
-        return {"1d3": 1, "2d5": self.nx, "2d5var": self.nx, "3d7": self.nx * self.ny}[self.family]
+        return {"1d3": 1, "1d3var": 1, "2d5": self.nx, "2d5var": self.nx,
+                "3d7": self.nx * self.ny, "3d7var": self.nx * self.ny}[self.family]
+
+
+VAR_FAMILIES = ("1d3var", "2d5var", "3d7var")
+DIMS = {"1d3": 1, "1d3var": 1, "2d5": 2, "2d5var": 2, "3d7": 3, "3d7var": 3}
+
+
+def face_shapes(family: str, dims) -> tuple:
+    """Expected face-array shapes of a variable-coefficient family (numpy
+    index order, slowest axis first): face_x couples x-neighbours (one more
+    face than points along x), face_y y-neighbours, face_z z-neighbours."""
+    if family == "1d3var":
+        (nx,) = dims
+        return ((nx + 1,),)
+    if family == "2d5var":
+        nx, ny = dims
+        return ((ny, nx + 1), (ny + 1, nx))
+    nx, ny, nz = dims
+    return ((nz, ny, nx + 1), (nz, ny + 1, nx), (nz + 1, ny, nx))
 
 
 class StencilOperator(DeviceOperator):
@@ -266,19 +289,20 @@ class StencilOperator(DeviceOperator):
 
     Constant coefficient ("1d3", "2d5", "3d7"): off-diagonals -dx2 and diagonal
     2d*dx2 with dx2 = (N+1)^2, as `poisson_1d` / `poisson_3d` assemble them
-    (reference problems.py:50-69,148-177).  Variable coefficient ("2d5var"):
-    `face_x` (ny, nx+1) and `face_y` (ny+1, nx) hold the dx2-scaled
-    harmonic-mean face coefficients; off-diagonals are -face and the diagonal is
-    ((c_w + c_e) + c_s) + c_n.  Face arrays are captured when the native handle
-    is created.
+    (reference problems.py:50-69,148-177).  Variable coefficient ("1d3var",
+    "2d5var", "3d7var"): `face_x` / `face_y` / `face_z` hold the dx2-scaled
+    face coefficients (shapes: `face_shapes`); off-diagonals are -face and the
+    diagonal is the sum of the point's faces in the order west, east, south,
+    north, bottom, top (2D: ((c_w + c_e) + c_s) + c_n).  Face arrays are
+    captured when the native handle is created.
     """
 
     def __init__(self, family: str, shape, dx2: float | None = None,
-                 face_x=None, face_y=None, device=None):
+                 face_x=None, face_y=None, device=None, face_z=None):
         if family not in FAMILIES:
             raise ValueError(f"unknown stencil family {family!r}")
         dims = tuple(int(v) for v in (shape if isinstance(shape, (tuple, list)) else (shape,)))
-        want = {"1d3": 1, "2d5": 2, "2d5var": 2, "3d7": 3}[family]
+        want = DIMS[family]
         if len(dims) != want or min(dims) < 1:
             raise ValueError(f"{family} needs {want} positive extents, got {shape!r}")
         self.family = family
@@ -287,15 +311,23 @@ class StencilOperator(DeviceOperator):
         self.n = self.grid.n
         self.halo = self.grid.halo
         self._init_device(device)
-        if family == "2d5var":
-            if face_x is None or face_y is None:
-                raise ValueError("variable-coefficient operator needs face_x and face_y")
-            nx, ny = dims
-            fx = np.asarray(face_x, dtype=np.float64) if isinstance(face_x, np.ndarray) else face_x
-            fy = np.asarray(face_y, dtype=np.float64) if isinstance(face_y, np.ndarray) else face_y
-            if tuple(fx.shape) != (ny, nx + 1) or tuple(fy.shape) != (ny + 1, nx):
-                raise ValueError("face arrays must be (ny, nx+1) and (ny+1, nx)")
-            self.face_x, self.face_y = fx, fy
+        self.face_x = self.face_y = self.face_z = None
+        if family in VAR_FAMILIES:
+            faces = (face_x, face_y, face_z)[:want]
+            if any(f is None for f in faces):
+                names = ("face_x", "face_y", "face_z")[:want]
+                raise ValueError(f"variable-coefficient operator needs {', '.join(names)}")
+            faces = [np.asarray(f, dtype=np.float64) if isinstance(f, np.ndarray) else f
+                     for f in faces]
+            shapes = face_shapes(family, dims)
+            for f, shp in zip(faces, shapes):
+                if tuple(f.shape) != shp:
+                    raise ValueError(f"face arrays must have shapes {shapes}")
+            self.face_x = faces[0]
+            if want >= 2:
+                self.face_y = faces[1]
+            if want == 3:
+                self.face_z = faces[2]
             self.dx2 = None
         else:
             if dx2 is None:
@@ -303,8 +335,11 @@ class StencilOperator(DeviceOperator):
             if not dx2 > 0.0:
                 raise ValueError("dx2 must be positive")
             self.dx2 = float(dx2)
-            self.face_x = self.face_y = None
         self._diag = None
+
+    @property
+    def is_var(self) -> bool:
+        return self.family in VAR_FAMILIES
 
     # ------------------------------------------------------------ SparseMatrix surface
     @property
@@ -319,6 +354,15 @@ class StencilOperator(DeviceOperator):
                 fx = _as_numpy(self.face_x)
                 fy = _as_numpy(self.face_y)
                 self._diag = (((fx[:, :-1] + fx[:, 1:]) + fy[:-1, :]) + fy[1:, :]).reshape(-1)
+            elif self.family == "3d7var":
+                fx = _as_numpy(self.face_x)
+                fy = _as_numpy(self.face_y)
+                fz = _as_numpy(self.face_z)
+                self._diag = (((((fx[:, :, :-1] + fx[:, :, 1:]) + fy[:, :-1, :]) + fy[:, 1:, :])
+                               + fz[:-1]) + fz[1:]).reshape(-1)
+            elif self.family == "1d3var":
+                fx = _as_numpy(self.face_x)
+                self._diag = fx[:-1] + fx[1:]
             else:
                 self._diag = np.full(self.n, self.diag_value)
         return self._diag
@@ -341,15 +385,18 @@ class StencilOperator(DeviceOperator):
         ids = np.arange(self.n).reshape(g.nz, g.ny, g.nx)
         diag = self.diag
         rows, cols, vals = [ids.reshape(-1)], [ids.reshape(-1)], [diag]
-        if self.family == "2d5var":
-            fx = _as_numpy(self.face_x)
-            fy = _as_numpy(self.face_y)
-            inner_x = fx[:, 1:-1]          # faces between i and i+1
-            inner_y = fy[1:-1, :]          # faces between j and j+1
-            a = ids[0, :, :-1].reshape(-1); b = ids[0, :, 1:].reshape(-1)
-            rows += [a, b]; cols += [b, a]; vals += [-inner_x.reshape(-1)] * 2
-            a = ids[0, :-1, :].reshape(-1); b = ids[0, 1:, :].reshape(-1)
-            rows += [a, b]; cols += [b, a]; vals += [-inner_y.reshape(-1)] * 2
+        if self.is_var:
+            # inner faces of each axis (numpy axis 2 = x, 1 = y, 0 = z)
+            faces = {2: self.face_x, 1: self.face_y, 0: self.face_z}
+            for axis in (2, 1, 0):
+                if ids.shape[axis] < 2 or faces[axis] is None:
+                    continue
+                f = _as_numpy(faces[axis]).reshape(
+                    tuple(ids.shape[a] + (1 if a == axis else 0) for a in range(3)))
+                inner = np.take(f, np.arange(1, ids.shape[axis]), axis=axis).reshape(-1)
+                lo = np.take(ids, np.arange(ids.shape[axis] - 1), axis=axis).reshape(-1)
+                hi = np.take(ids, np.arange(1, ids.shape[axis]), axis=axis).reshape(-1)
+                rows += [lo, hi]; cols += [hi, lo]; vals += [-inner] * 2
         else:
             off = -1.0 * self.dx2
             for axis in (2, 1, 0):
@@ -363,8 +410,8 @@ class StencilOperator(DeviceOperator):
     @property
     def planes(self) -> int:
         """Planes along the slab axis (z in 3D, rows in 2D, 1 in 1D)."""
-        return {"1d3": 1, "2d5": self.shape[1], "2d5var": self.shape[1],
-                "3d7": self.shape[2]}[self.family]
+        return {"1d3": 1, "1d3var": 1, "2d5": self.shape[1], "2d5var": self.shape[1],
+                "3d7": self.shape[2], "3d7var": self.shape[2]}[self.family]
 
     # ------------------------------------------------------------ device side
     def _fill_desc(self, desc, dev) -> None:
@@ -372,11 +419,15 @@ class StencilOperator(DeviceOperator):
         desc.family = FAMILIES[self.family]
         desc.nx, desc.ny, desc.nz = g.nx, g.ny, g.nz
         desc.dx2 = self.dx2 if self.dx2 is not None else 0.0
-        if self.family == "2d5var":
-            fx = _to_device(self.face_x, dev).contiguous()
-            fy = _to_device(self.face_y, dev).contiguous()
-            self._keep = (fx, fy)
-            desc.face_x, desc.face_y = fx.data_ptr(), fy.data_ptr()
+        if self.is_var:
+            keep = []
+            for name in ("face_x", "face_y", "face_z"):
+                f = getattr(self, name)
+                if f is not None:
+                    t = _to_device(f, dev).contiguous()
+                    keep.append(t)
+                    setattr(desc, name, t.data_ptr())
+            self._keep = tuple(keep)
 
 
 def _as_numpy(a) -> np.ndarray:

@@ -184,6 +184,82 @@ def gaussian_field(n: int, seed: int) -> np.ndarray:
     return s / 9.0
 
 
+def _normals(seed: int, cnt: int) -> np.ndarray:
+    """cnt i.i.d. N(0,1) by Box-Muller from SplitMix64(derive_seed(seed,
+    FIELD_WORD)) uniforms taken in pairs (as gaussian_field)."""
+    u = uniforms_counter(derive_seed(seed, FIELD_WORD), 2 * ((cnt + 1) // 2))
+    u1, u2 = u[0::2], u[1::2]
+    rad = np.sqrt(-2.0 * np.log1p(-u1))
+    ang = 2.0 * np.pi * u2
+    xi = np.empty(2 * u1.size)
+    xi[0::2] = rad * np.cos(ang)
+    xi[1::2] = rad * np.sin(ang)
+    return xi[:cnt]
+
+
+BOX3 = 5          # 3D box filter width (5 x 5 x 5)
+PAD3 = BOX3 // 2
+
+
+def gaussian_field_3d(n: int, seed: int) -> np.ndarray:
+    """g on the (n+2)^3 node grid (z slowest, x fastest) for the 3D
+    variable-coefficient problem: xi i.i.d. N(0,1) (`_normals`, x fastest) on
+    an (n+2+2*PAD3)^3 grid, g = (5x5x5 box sum of xi) / sqrt(125), summed
+    along x first, then y, then z, each left to right (unit variance)."""
+    m = n + 2 + 2 * PAD3
+    o = m - 2 * PAD3
+    xi = _normals(seed, m * m * m).reshape(m, m, m)
+    sx = xi[:, :, 0:o].copy()
+    for d in range(1, BOX3):
+        sx += xi[:, :, d:d + o]
+    del xi
+    sy = sx[:, 0:o, :].copy()
+    for d in range(1, BOX3):
+        sy += sx[:, d:d + o, :]
+    del sx
+    s = sy[0:o].copy()
+    for d in range(1, BOX3):
+        s += sy[d:d + o]
+    del sy
+    s /= np.sqrt(125.0)
+    return s
+
+
+def gaussian_field_1d(n: int, seed: int) -> np.ndarray:
+    """g on the n+2 nodes of the 1D variable-coefficient problem: xi
+    (`_normals`) on n+2+2*PAD nodes, g = (9-point box sum, left to right) / 3."""
+    m = n + 2 + 2 * PAD
+    xi = _normals(seed, m)
+    s = xi[0:m - 2 * PAD].copy()
+    for d in range(1, BOX):
+        s = s + xi[d:d + m - 2 * PAD]
+    return s / 3.0
+
+
+def _hm(a, b, dx2):
+    return (2.0 * a * b) / (a + b) * dx2
+
+
+def harmonic_faces_3d(k: np.ndarray, dx2: float):
+    """dx2-scaled harmonic-mean faces from the (n+2)^3 node coefficients
+    (index [z, y, x], boundary nodes included): face_x[z, j, i] couples x-nodes
+    i-1 and i of interior row (j, z) (i = 0 and i = nx are boundary faces);
+    face_y[z, j, i] couples rows j-1 and j; face_z[z, j, i] planes z-1 and z."""
+    c = k[1:-1, 1:-1, :]
+    face_x = _hm(c[:, :, :-1], c[:, :, 1:], dx2)
+    c = k[1:-1, :, 1:-1]
+    face_y = _hm(c[:, :-1, :], c[:, 1:, :], dx2)
+    c = k[:, 1:-1, 1:-1]
+    face_z = _hm(c[:-1], c[1:], dx2)
+    return (np.ascontiguousarray(face_x), np.ascontiguousarray(face_y),
+            np.ascontiguousarray(face_z))
+
+
+def harmonic_faces_1d(k: np.ndarray, dx2: float) -> np.ndarray:
+    """face_x[i] couples nodes i-1 and i of the n+2 node coefficients."""
+    return np.ascontiguousarray(_hm(k[:-1], k[1:], dx2))
+
+
 def harmonic_faces(k: np.ndarray, dx2: float) -> tuple[np.ndarray, np.ndarray]:
     """dx2-scaled harmonic-mean faces from the (n+2)^2 node coefficients.
 
@@ -211,6 +287,33 @@ def diffusion_2d_varcoef(n: int, seed: int = 0, device=None) -> ProblemInstance:
                            stopping_norm=RELATIVE_L2, label=f"varcoef2d:{n}:seed{seed}")
 
 
+def diffusion_3d_varcoef(n: int, seed: int = 0, device=None) -> ProblemInstance:
+    """-div(k grad u) = f on n^3 interior points, 7-point stencil with
+    harmonic-mean faces, k = exp(g) (`gaussian_field_3d`), Dirichlet, f and
+    x0 as the BASELINE recipe (north_star: 3D variable-coefficient stencil)."""
+    if n < 2:
+        raise ValueError("n must be at least 2")
+    dx2 = (n + 1.0) ** 2
+    fx, fy, fz = harmonic_faces_3d(np.exp(gaussian_field_3d(n, seed)), dx2)
+    A = StencilOperator("3d7var", (n, n, n), face_x=fx, face_y=fy, face_z=fz, device=device)
+    N = n ** 3
+    return ProblemInstance(A=A, b=uniform_rhs(seed, N), x0=np.zeros(N),
+                           stopping_norm=RELATIVE_L2, label=f"varcoef3d:{n}:seed{seed}")
+
+
+def diffusion_1d_varcoef(n: int, seed: int = 0, device=None) -> ProblemInstance:
+    """-(k u')' = f on n interior points, 3-point stencil with harmonic-mean
+    faces, k = exp(g) (`gaussian_field_1d`), Dirichlet (north_star: 1D
+    variable-coefficient stencil)."""
+    if n < 2:
+        raise ValueError("n must be at least 2")
+    dx2 = (n + 1.0) ** 2
+    fx = harmonic_faces_1d(np.exp(gaussian_field_1d(n, seed)), dx2)
+    A = StencilOperator("1d3var", (n,), face_x=fx, device=device)
+    return ProblemInstance(A=A, b=uniform_rhs(seed, n), x0=np.zeros(n),
+                           stopping_norm=RELATIVE_L2, label=f"varcoef1d:{n}:seed{seed}")
+
+
 # ---------------------------------------------------------------------------
 # BASELINE.json configs
 # ---------------------------------------------------------------------------
@@ -222,6 +325,10 @@ CONFIGS = {
     "c3": ("3d7", 512, "3D Poisson 512^3"),
     "c4": ("2d5var", 4096, "2D variable-coefficient diffusion 4096^2"),
     "c5": ("3d7", 1024, "3D Poisson 1024^3"),
+    # north_star's variable-coefficient stencils in 3D and 1D (not BASELINE
+    # configs: same recipe as C3 / C1 with k = exp(g) faces)
+    "c3v": ("3d7var", 512, "3D variable-coefficient diffusion 512^3"),
+    "c1v": ("1d3var", 1024, "1D variable-coefficient diffusion N=1024"),
 }
 
 
@@ -231,6 +338,10 @@ def baseline_problem(family: str, n: int, seed: int = 0, device=None,
     relative L2 stopping norm."""
     if family == "2d5var":
         return diffusion_2d_varcoef(n, seed, device=device)
+    if family == "3d7var":
+        return diffusion_3d_varcoef(n, seed, device=device)
+    if family == "1d3var":
+        return diffusion_1d_varcoef(n, seed, device=device)
     dims = {"1d3": (n,), "2d5": (n, n), "3d7": (n, n, n)}[family]
     A = StencilOperator(family, dims, dx2=(n + 1.0) ** 2, device=device)
     N = A.n

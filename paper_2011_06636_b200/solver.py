@@ -27,6 +27,7 @@ import numpy as np
 from . import _lib
 from .operators import DeviceOperator, Field, StencilOperator
 from .problems import ABSOLUTE_L2, RELATIVE_L2, SOLUTION_DIFF_INF, ProblemInstance
+from .sparse import device_operator
 from .schemes import (MAX_LEVEL, ORDER_GRID_SIZE, SrjScheme, generate_srj_scheme,
                       scheme_for_level)
 
@@ -50,12 +51,8 @@ class StoppingRule:
 
 
 class ResidualKnown:
-    """`SolverState.cached_r` marker: the residual of `x` is `current_residual`.
-
-    The reference caches the vector r = b - A x (solver.py:53-54,205-207); the
-    device path never materialises r (every sweep recomputes it from x), so the
-    state only needs to know that `current_residual` belongs to `x`.
-    """
+    """Internal `SolverState.cached_r` marker of the solve loop: the residual of
+    `x` is `current_residual` (the device path never needs the vector r)."""
 
     __slots__ = ()
 
@@ -64,6 +61,24 @@ class ResidualKnown:
 
 
 RESIDUAL_KNOWN = ResidualKnown()
+
+
+class LazyResidual:
+    """r = b - A x of a run_cycle result, materialised on first access of
+    `SolverState.cached_r` (reference solver.py:205-210,270 keep that vector).
+    One device matvec plus one subtraction: bit-identical to the reference's
+    `b - csr.dot(x)`."""
+
+    __slots__ = ("_A", "_b", "_x", "_as_numpy")
+
+    def __init__(self, A, b, x, as_numpy: bool):
+        self._A, self._b, self._x, self._as_numpy = A, b, x, as_numpy
+
+    def materialize(self):
+        A = self._A
+        y = A.matvec(A.field(self._x))
+        r = self._b.interior - y
+        return r.cpu().numpy() if self._as_numpy else r
 
 
 @dataclass
@@ -77,6 +92,31 @@ class SolverState:
     current_residual: float | None = None
     cached_r: object | None = None
     converged: bool = False
+
+
+def _get_cached_r(self):
+    r = self.__dict__.get("_cached_r")
+    if isinstance(r, LazyResidual):
+        r = r.materialize()
+        self.__dict__["_cached_r"] = r
+    elif isinstance(r, ResidualKnown):
+        return None
+    return r
+
+
+def _set_cached_r(self, value):
+    self.__dict__["_cached_r"] = value
+
+
+SolverState.cached_r = property(_get_cached_r, _set_cached_r)
+
+
+def _residual_known(state) -> bool:
+    """Whether `state` carries the residual of its x (without materialising a
+    LazyResidual); works for the reference's own SolverState too."""
+    if "_cached_r" in getattr(state, "__dict__", {}):
+        return state.__dict__["_cached_r"] is not None
+    return getattr(state, "cached_r", None) is not None
 
 
 @dataclass(frozen=True)
@@ -289,14 +329,6 @@ def _solve_on_device(A: StencilOperator, b: Field, x: Field, x_alt: Field, contr
     )
 
 
-def _require_device_operator(A) -> DeviceOperator:
-    if not isinstance(A, DeviceOperator):
-        raise TypeError(
-            "the SRJ device path needs a device operator (StencilOperator or "
-            f"sparse.SparseMatrix); got {type(A).__name__}")
-    return A
-
-
 def _l2_norm_parts(norm: str) -> None:
     if norm not in (ABSOLUTE_L2, RELATIVE_L2, SOLUTION_DIFF_INF):
         raise ValueError(f"unknown norm {norm!r}")
@@ -362,7 +394,7 @@ def _device_cycle(A: DeviceOperator, b: Field, x: Field, x_alt: Field, state: So
     """
     if norm == SOLUTION_DIFF_INF:
         return _diff_cycle(A, b, x, x_alt, state, scheme, stopping, record_history, x_out_kind)
-    if state.cached_r is not None and state.current_residual is not None:
+    if _residual_known(state) and state.current_residual is not None:
         res_now = float(state.current_residual)
     else:
         res_now = math.sqrt(A.residual_sq(x, b)) / baseline
@@ -427,7 +459,7 @@ def run_cycle(A: StencilOperator, b, state: SolverState, scheme: SrjScheme,
     The input state is not modified (its x is copied into a fresh device
     ping-pong pair); numpy inputs give numpy outputs.
     """
-    A = _require_device_operator(A)
+    A = device_operator(A)
     if stopping is not None and norm != stopping.norm:
         norm = stopping.norm
     _l2_norm_parts(norm)
@@ -441,6 +473,8 @@ def run_cycle(A: StencilOperator, b, state: SolverState, scheme: SrjScheme,
 
     new_state, stats, _, _ = _device_cycle(A, bf, x, x_alt, state, scheme, stopping,
                                            baseline, record_history, kind, norm)
+    if norm != SOLUTION_DIFF_INF:
+        new_state.cached_r = LazyResidual(A, bf, new_state.x, as_numpy)
     return new_state, stats
 
 
@@ -470,7 +504,7 @@ def solve(problem: ProblemInstance, controller: Controller, stopping: StoppingRu
     do not allocate a fresh host buffer each time.
     """
     t0 = time.perf_counter()
-    A = _require_device_operator(problem.A)
+    A = device_operator(problem.A)
     _l2_norm_parts(stopping.norm)
     b = A.field(problem.b)
     x = A.field(problem.x0)

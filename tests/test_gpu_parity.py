@@ -129,12 +129,11 @@ def test_solve_is_deterministic_on_device():
 TB_NAMES = [c["name"] for c in P.cases(lambda c: c["family"] == "2d5" and "diverged" not in c)]
 
 
-@pytest.mark.parametrize("kind", ["tile", "warp_stream"])
 @pytest.mark.parametrize("spp", [1, 2, 3, 5, 6, 8])
 @pytest.mark.parametrize("name", TB_NAMES)
-def test_temporal_blocking_matches_reference(name, spp, kind):
+def test_temporal_blocking_matches_reference(name, spp):
     c = P.case(name)
-    rep = device_solve(c, record_history="history" in c, sweeps_per_pass=spp, tb_kind=kind)
+    rep = device_solve(c, record_history="history" in c, sweeps_per_pass=spp)
     P.assert_trace_matches(c, rows_of(rep), rep.total_iterations, rep.converged, x=rep.x,
                            history=rep.residual_history if "history" in c else None)
 

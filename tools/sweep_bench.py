@@ -17,7 +17,6 @@ def main():
     ap.add_argument("cases")
     ap.add_argument("--level", type=int, default=20)
     ap.add_argument("--spp", type=int, default=0, help="sweeps per pass (0: operator default)")
-    ap.add_argument("--kind", default=None, help="2D temporal kernel: tile | warp_stream")
     ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
     import numpy as np
@@ -34,8 +33,6 @@ def main():
         A = p.A
         if a.spp > 0:
             A.set_sweeps_per_pass(a.spp)
-        if a.kind and fam == "2d5":
-            A.set_temporal_kernel(a.kind)
         b = A.field(p.b)
         x = A.new_field()
         xa = A.new_field()
