@@ -37,4 +37,21 @@ cudaError_t launch3d_cycle(const Plan3D& plan, const Geom& g, double* x, double*
                            double baseline, double* partials, double* hist, int* out_i,
                            double* out_d, cudaStream_t st);
 
+// Plane-streaming cycle kernel for the 3D 7-point VARIABLE-coefficient
+// stencil (srj_3dv.cu).  Owns a 16-byte-pitch copy of face_x.
+struct Plan3V {
+    bool supported = false;
+    int blocks = 0, per_sm = 0, slots = 0;
+    int tiles_x = 0, tiles_y = 0, zc = 0, nzc = 0, items = 0;
+    double* fx_pad = nullptr;  // face_x with row pitch nx + 2
+    int fx_pitch = 0;
+};
+
+cudaError_t plan3v_init(Plan3V& plan, const Geom& g, int num_sms);
+void plan3v_free(Plan3V& plan);
+cudaError_t launch3v_cycle(const Plan3V& plan, const Geom& g, double* x, double* x_alt,
+                           const double* b, const double* omegas, int M, double tol,
+                           double baseline, double* partials, double* hist, int* out_i,
+                           double* out_d, cudaStream_t st);
+
 }  // namespace srj

@@ -601,6 +601,7 @@ struct srj_op {
     Tb3Plan tb3;                 // 3D temporal-blocking plan (srj_tb3d.cu)
     TbvPlan tbv;                 // var-coef 2D temporal-blocking plan (srj_tbvar.cu)
     Plan3D p3;                   // plane-streaming 3D plan (srj_3d.cuh)
+    Plan3V p3v;                  // plane-streaming 3D variable-coefficient plan (srj_3dv.cu)
     Plan2D p2;                   // tile-streaming 2D plan (srj_2d.cuh)
     // srj_sweep_planes scratch, one set per slot (concurrent launches)
     double* slot_part[kSlots] = {nullptr, nullptr};
@@ -747,6 +748,10 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("3D plan setup failed: ") + cudaGetErrorString(e));
     }
+    if ((e = plan3v_init(op->p3v, g, op->num_sms)) != cudaSuccess) {
+        srj_op_destroy(op);
+        return fail(SRJ_CUDA_ERROR, std::string("3D var-coef plan setup failed: ") + cudaGetErrorString(e));
+    }
     if ((e = tb_plan_init(op->tb, g, op->num_sms)) != cudaSuccess) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("temporal-blocking setup failed: ") + cudaGetErrorString(e));
@@ -804,6 +809,7 @@ int srj_op_destroy(srj_op* op) {
     cudaFree(op->solve_hist);
     plan2d_free(op->p2);
     tbv_plan_free(op->tbv);
+    plan3v_free(op->p3v);
     delete op;
     return SRJ_OK;
 }
@@ -849,6 +855,7 @@ int srj_op_describe(const srj_op* op, srj_op_info* info) {
     info->cycle_kernel = (op->sweeps_per_pass > 1 && op->tbv.supported)  ? SRJ_KERNEL_TBVAR
                          : (op->sweeps_per_pass > 1 && op->tb3.supported) ? SRJ_KERNEL_TB3D
                          : op->p3.supported                               ? SRJ_KERNEL_PLANE3D
+                         : op->p3v.supported                              ? SRJ_KERNEL_PLANE3DV
                          : (op->sweeps_per_pass > 1 && op->tb.supported) ? SRJ_KERNEL_TB2D
                          : op->p2.supported                               ? SRJ_KERNEL_TILE2D
                          : reg1d_ok(op->g) ? SRJ_KERNEL_REG1D
@@ -908,6 +915,9 @@ int srj_residual_sq(srj_op* op, const double* x, const double* b, double* sumsq_
     if (op->p3.supported) {
         CUDA_TRY(launch3d_cycle(op->p3, op->g, const_cast<double*>(x), nullptr, b, nullptr, 0, 0.0,
                                 1.0, op->partials, op->hist, op->out_i, op->out_d, st));
+    } else if (op->p3v.supported) {
+        CUDA_TRY(launch3v_cycle(op->p3v, op->g, const_cast<double*>(x), nullptr, b, nullptr, 0, 0.0,
+                                1.0, op->partials, op->hist, op->out_i, op->out_d, st));
     } else if (op->p2.supported) {
         CUDA_TRY(launch2d_cycle(op->p2, op->g, const_cast<double*>(x), nullptr, b, nullptr, 0, 0.0,
                                 1.0, op->partials, op->hist, op->out_i, op->out_d, st));
@@ -952,6 +962,10 @@ int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
         CUDA_TRY(tb3_launch_cycle(op->tb3, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,
                                   op->partials, op->hist, op->out_i, op->out_d, st, 0, op->g.nz,
                                   nullptr));
+        out->launches = 1;
+    } else if (op->p3v.supported) {
+        CUDA_TRY(launch3v_cycle(op->p3v, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,
+                                op->partials, op->hist, op->out_i, op->out_d, st));
         out->launches = 1;
     } else if (op->p3.supported) {
         CUDA_TRY(launch3d_cycle(op->p3, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,

@@ -63,4 +63,13 @@ cudaError_t encode_volume_map(CUtensorMap* map, const double* base, int nx, int 
     return encode(map, base, 3, dims, strides, box);
 }
 
+cudaError_t encode_volume_map_pitched(CUtensorMap* map, const double* base, int width, int rows,
+                                      int planes, int pitch, int box_x, int box_y) {
+    const cuuint64_t dims[3] = {(cuuint64_t)width, (cuuint64_t)rows, (cuuint64_t)planes};
+    const cuuint64_t strides[2] = {(cuuint64_t)pitch * sizeof(double),
+                                   (cuuint64_t)pitch * rows * sizeof(double)};
+    const cuuint32_t box[3] = {(cuuint32_t)box_x, (cuuint32_t)box_y, 1};
+    return encode(map, base, 3, dims, strides, box);
+}
+
 }  // namespace srj

@@ -114,4 +114,10 @@ cudaError_t encode_field_map_pitched(CUtensorMap* map, const double* base, int w
 cudaError_t encode_volume_map(CUtensorMap* map, const double* base, int nx, int ny, int nz,
                               int box_x, int box_y);
 
+// Host: 3D fp64 map over `planes` planes of `rows` rows of `width` valid
+// values, row pitch `pitch` doubles (pitch*8 a multiple of 16), plane pitch
+// pitch*rows; box of box_x x box_y x 1, zero fill out of bounds.
+cudaError_t encode_volume_map_pitched(CUtensorMap* map, const double* base, int width, int rows,
+                                      int planes, int pitch, int box_x, int box_y);
+
 }  // namespace srj

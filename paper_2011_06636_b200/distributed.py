@@ -67,18 +67,19 @@ class SlabLayout:
     world: int
 
     def __post_init__(self):
-        if self.family == "1d3" and self.world != 1:
+        if self.family in ("1d3", "1d3var") and self.world != 1:
             raise ValueError("a 1D grid is not sharded (replicas only)")
         if self.world < 1 or self.world > self.planes:
             raise ValueError(f"{self.world} slabs for {self.planes} planes")
 
     @property
     def planes(self) -> int:
-        return 1 if self.family == "1d3" else int(self.shape[-1])
+        return 1 if self.family in ("1d3", "1d3var") else int(self.shape[-1])
 
     @property
     def plane_points(self) -> int:
-        return int(np.prod(self.shape[:-1])) if self.family != "1d3" else int(self.shape[0])
+        return (int(np.prod(self.shape[:-1])) if self.family not in ("1d3", "1d3var")
+                else int(self.shape[0]))
 
     @property
     def n(self) -> int:
@@ -91,7 +92,7 @@ class SlabLayout:
         return start, count
 
     def local_shape(self, rank: int) -> tuple:
-        if self.family == "1d3":
+        if self.family in ("1d3", "1d3var"):
             return tuple(self.shape)
         return tuple(self.shape[:-1]) + (self.span(rank)[1],)
 
@@ -101,17 +102,26 @@ class Slab:
     and the cycle-start snapshot (all Fields with ghost planes)."""
 
     def __init__(self, layout: SlabLayout, rank: int, device, dx2: float | None = None,
-                 face_x=None, face_y=None):
+                 face_x=None, face_y=None, face_z=None):
         self.layout = layout
         self.rank = rank
         self.start, self.count = layout.span(rank)
         nx = layout.shape[0]
-        if dx2 is None and layout.family != "2d5var":
+        lo, hi = self.start, self.start + self.count
+        if dx2 is None and layout.family not in ("2d5var", "3d7var", "1d3var"):
             dx2 = (nx + 1.0) ** 2
         if layout.family == "2d5var":
-            fx = face_x[self.start:self.start + self.count, :]
-            fy = face_y[self.start:self.start + self.count + 1, :]
+            fx = face_x[lo:hi, :]
+            fy = face_y[lo:hi + 1, :]
             self.A = StencilOperator("2d5var", layout.local_shape(rank), face_x=fx, face_y=fy,
+                                     device=device)
+        elif layout.family == "3d7var":
+            # z-slab: its planes' x/y faces and the nz+1 z-faces bounding them
+            self.A = StencilOperator("3d7var", layout.local_shape(rank), face_x=face_x[lo:hi],
+                                     face_y=face_y[lo:hi], face_z=face_z[lo:hi + 1],
+                                     device=device)
+        elif layout.family == "1d3var":
+            self.A = StencilOperator("1d3var", layout.local_shape(rank), face_x=face_x,
                                      device=device)
         else:
             self.A = StencilOperator(layout.family, layout.local_shape(rank), dx2=dx2,
@@ -129,7 +139,7 @@ class Slab:
 
     @property
     def planes(self) -> int:
-        return self.count if self.layout.family != "1d3" else 1
+        return self.count if self.layout.family not in ("1d3", "1d3var") else 1
 
     def swap(self) -> None:
         self.x, self.x_alt = self.x_alt, self.x
@@ -430,9 +440,10 @@ class SlabSolver:
 
 
 def local_slabs(family: str, shape, world: int, ranks, device, face_x=None, face_y=None,
-                dx2: float | None = None) -> list[Slab]:
+                dx2: float | None = None, face_z=None) -> list[Slab]:
     layout = SlabLayout(family, tuple(shape), world)
-    return [Slab(layout, r, device, dx2=dx2, face_x=face_x, face_y=face_y) for r in ranks]
+    return [Slab(layout, r, device, dx2=dx2, face_x=face_x, face_y=face_y, face_z=face_z)
+            for r in ranks]
 
 
 # ---------------------------------------------------------------------------

@@ -55,24 +55,65 @@ def sha(x) -> str:
     return hashlib.sha256(np.ascontiguousarray(x, dtype=np.float64).tobytes()).hexdigest()
 
 
-def case_inputs(c):
-    """(family, n, b, face_x, face_y) for a golden case, built from the
-    product-independent recipes (SplitMix64 rhs; config-4 faces)."""
+DIMS = {"1d3": 1, "1d3var": 1, "2d5": 2, "2d5var": 2, "3d7": 3, "3d7var": 3}
+
+
+def case_faces(c) -> dict:
+    """Face arrays of a variable-coefficient golden case (product-independent
+    recipes: problems.gaussian_field* / harmonic_faces*), checked against the
+    sha256 the golden script recorded; {} for constant coefficients."""
     import sys
     root = os.path.dirname(HERE)
     if root not in sys.path:
         sys.path.insert(0, root)
-    from paper_2011_06636_b200.problems import gaussian_field, harmonic_faces
+    from paper_2011_06636_b200 import problems as pr
+    fam, n, seed = c["family"], c["n"], c.get("seed", 0)
+    key = (fam, n, seed)
+    if key in _cache:
+        return _cache[key]
+    dx2 = (n + 1.0) ** 2
+    if fam == "2d5var":
+        fx, fy = pr.harmonic_faces(np.exp(pr.gaussian_field(n, seed)), dx2)
+        faces = {"face_x": fx, "face_y": fy}
+    elif fam == "3d7var":
+        fx, fy, fz = pr.harmonic_faces_3d(np.exp(pr.gaussian_field_3d(n, seed)), dx2)
+        faces = {"face_x": fx, "face_y": fy, "face_z": fz}
+    elif fam == "1d3var":
+        faces = {"face_x": pr.harmonic_faces_1d(np.exp(pr.gaussian_field_1d(n, seed)), dx2)}
+    else:
+        faces = {}
+    for k, v in faces.items():
+        assert sha(v) == c[f"{k}_sha256"], (c["name"], k)
+    _cache[key] = faces
+    return faces
+
+
+def case_inputs(c):
+    """(family, n, b, face_x, face_y) for a golden case, built from the
+    product-independent recipes (SplitMix64 rhs; config-4 faces).  3D
+    variable coefficient: face_z from `case_faces`."""
+    import sys
+    root = os.path.dirname(HERE)
+    if root not in sys.path:
+        sys.path.insert(0, root)
     from paper_2011_06636_b200.rng import uniform_rhs
 
     fam, n = c["family"], c["n"]
-    N = {"1d3": n, "2d5": n * n, "2d5var": n * n, "3d7": n ** 3}[fam]
+    N = n ** DIMS[fam]
     b = np.ones(N) if c.get("rhs", "uniform") == "ones" else uniform_rhs(c.get("seed", 0), N)
-    fx = fy = None
-    if fam == "2d5var":
-        fx, fy = harmonic_faces(np.exp(gaussian_field(n, c.get("seed", 0))), (n + 1.0) ** 2)
-        assert sha(fx) == c["face_x_sha256"] and sha(fy) == c["face_y_sha256"]
-    return fam, n, b, fx, fy
+    faces = case_faces(c)
+    return fam, n, b, faces.get("face_x"), faces.get("face_y")
+
+
+def case_operator(c, device=None):
+    """The product's StencilOperator of a structured golden case."""
+    import sys
+    root = os.path.dirname(HERE)
+    if root not in sys.path:
+        sys.path.insert(0, root)
+    from paper_2011_06636_b200.operators import StencilOperator
+    fam, n = c["family"], c["n"]
+    return StencilOperator(fam, (n,) * DIMS[fam], device=device, **case_faces(c))
 
 
 def is_csr(c) -> bool:

@@ -33,7 +33,9 @@ import srj  # noqa: E402  (the reference)
 from srj.problems import ProblemInstance  # noqa: E402
 from srj.sparse import SparseMatrix  # noqa: E402
 
-from paper_2011_06636_b200.problems import gaussian_field, harmonic_faces  # noqa: E402
+from paper_2011_06636_b200.problems import (gaussian_field, gaussian_field_1d,  # noqa: E402
+                                            gaussian_field_3d, harmonic_faces,
+                                            harmonic_faces_1d, harmonic_faces_3d)
 from paper_2011_06636_b200.rng import uniform_rhs  # noqa: E402
 
 MAX_X_STORE = 4096
@@ -73,6 +75,37 @@ def varcoef_2d_ref(n: int, seed: int):
     return A, sha(fx), sha(fy)
 
 
+def varcoef_3d_ref(n: int, seed: int):
+    """3D 7-point variable-coefficient CSR for the reference: off-diagonals
+    -face, diagonal (((((c_w + c_e) + c_s) + c_n) + c_b) + c_t) (srj.h)."""
+    dx2 = (n + 1.0) ** 2
+    fx, fy, fz = harmonic_faces_3d(np.exp(gaussian_field_3d(n, seed)), dx2)
+    ids = np.arange(n ** 3).reshape(n, n, n)
+    diag = (((((fx[:, :, :-1] + fx[:, :, 1:]) + fy[:, :-1, :]) + fy[:, 1:, :]) + fz[:-1])
+            + fz[1:]).ravel()
+    rows, cols, vals = [ids.ravel()], [ids.ravel()], [diag]
+    for (a, b), v in (((ids[:, :, :-1], ids[:, :, 1:]), -fx[:, :, 1:-1]),
+                      ((ids[:, :-1, :], ids[:, 1:, :]), -fy[:, 1:-1, :]),
+                      ((ids[:-1], ids[1:]), -fz[1:-1])):
+        rows += [a.ravel(), b.ravel()]
+        cols += [b.ravel(), a.ravel()]
+        vals += [v.ravel()] * 2
+    A = SparseMatrix.from_coo(n ** 3, np.concatenate(rows), np.concatenate(cols),
+                              np.concatenate(vals))
+    return A, {"face_x_sha256": sha(fx), "face_y_sha256": sha(fy), "face_z_sha256": sha(fz)}
+
+
+def varcoef_1d_ref(n: int, seed: int):
+    dx2 = (n + 1.0) ** 2
+    fx = harmonic_faces_1d(np.exp(gaussian_field_1d(n, seed)), dx2)
+    ids = np.arange(n)
+    rows = [ids, ids[:-1], ids[1:]]
+    cols = [ids, ids[1:], ids[:-1]]
+    vals = [fx[:-1] + fx[1:], -fx[1:-1], -fx[1:-1]]
+    A = SparseMatrix.from_coo(n, np.concatenate(rows), np.concatenate(cols), np.concatenate(vals))
+    return A, {"face_x_sha256": sha(fx)}
+
+
 def build_csr(case):
     """General-CSR problems (§8 f2/f3) through the reference's own generators."""
     fam = case["family"]
@@ -110,6 +143,10 @@ def build(case):
         A = p.A
     elif fam == "2d5":
         A = poisson_2d_ref(n)
+    elif fam == "3d7var":
+        A, extra = varcoef_3d_ref(n, seed)
+    elif fam == "1d3var":
+        A, extra = varcoef_1d_ref(n, seed)
     else:
         A, hx, hy = varcoef_2d_ref(n, seed)
         extra = {"face_x_sha256": hx, "face_y_sha256": hy}
@@ -285,6 +322,26 @@ CASES = [
 ]
 
 
+# north_star's 1D / 3D variable-coefficient stencils (round 2): merged into
+# traces.json by `make_golden.py --var` without re-running the cases above
+VAR_CASES = [
+    {"name": "c3v_12", "family": "3d7var", "n": 12, "seed": 0, "norm": "relative_l2",
+     "tol": 1e-8, "controller": "heuristic", "history": True},
+    {"name": "c3v_20", "family": "3d7var", "n": 20, "seed": 3, "norm": "relative_l2",
+     "tol": 1e-8, "controller": "heuristic"},
+    {"name": "c3v_31", "family": "3d7var", "n": 31, "seed": 1, "norm": "relative_l2",
+     "tol": 1e-8, "controller": "heuristic"},
+    {"name": "c3v_32", "family": "3d7var", "n": 32, "seed": 0, "norm": "relative_l2",
+     "tol": 1e-8, "controller": "heuristic"},
+    {"name": "c3v_24_budget", "family": "3d7var", "n": 24, "seed": 4, "norm": "relative_l2",
+     "tol": 1e-8, "controller": "heuristic", "max_iterations": 150},
+    {"name": "c1v_1024", "family": "1d3var", "n": 1024, "seed": 0, "norm": "relative_l2",
+     "tol": 1e-8, "controller": "heuristic", "history": True},
+    {"name": "c1v_100_s2", "family": "1d3var", "n": 100, "seed": 2, "norm": "relative_l2",
+     "tol": 1e-8, "controller": "heuristic"},
+]
+
+
 def datacollect_cases():
     """Reference data collection (datacollect.py:79-147) and the threshold fit."""
     from srj import datacollect as dc
@@ -307,6 +364,20 @@ def datacollect_cases():
     return out
 
 
+def main_var():
+    path = os.path.join(HERE, "traces.json")
+    with open(path) as fh:
+        traces = json.load(fh)
+    names = {c["name"] for c in VAR_CASES}
+    traces["cases"] = [c for c in traces["cases"] if c["name"] not in names]
+    for case in VAR_CASES:
+        print("running", case["name"], flush=True)
+        traces["cases"].append(run_case(case))
+    with open(path, "w") as fh:
+        json.dump(traces, fh, separators=(",", ":"))
+    print("merged", len(VAR_CASES), "cases into", path)
+
+
 def main():
     traces = {"reference": "/root/reference (srj 0.1.0)", "numpy": np.__version__,
               "cases": [], "run_cycle": run_cycle_cases(), "datacollect": datacollect_cases()}
@@ -325,4 +396,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "--var" in sys.argv[1:]:
+        main_var()
+    else:
+        main()

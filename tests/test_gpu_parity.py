@@ -28,12 +28,8 @@ def device_solve(c, record_history=True, sweeps_per_pass=None, tb_kind=None):
         A = srj.SparseMatrix(csr, device=dev)
         n = A.n
     else:
-        fam, n, b, fx, fy = P.case_inputs(c)
-        dims = {"1d3": (n,), "2d5": (n, n), "2d5var": (n, n), "3d7": (n, n, n)}[fam]
-        if fam == "2d5var":
-            A = srj.StencilOperator(fam, dims, face_x=fx, face_y=fy, device=dev)
-        else:
-            A = srj.StencilOperator(fam, dims, device=dev)
+        fam, n, b, _, _ = P.case_inputs(c)
+        A = P.case_operator(c, device=dev)
         x0 = np.zeros(A.n)
     if sweeps_per_pass:
         A.set_sweeps_per_pass(sweeps_per_pass)

@@ -31,9 +31,16 @@ def _oracle_sweeps(op, x, b, omegas, baseline):
 
 def _case(family, seed):
     rng = np.random.default_rng(1000 * seed + {"1d3": 1, "2d5": 2, "2d5var": 3, "3d7": 4,
-                                               "3d7big": 5}[family])
-    if family == "1d3":
+                                               "3d7big": 5, "3d7var": 6, "3d7varbig": 7,
+                                               "1d3var": 8}[family])
+    if family in ("1d3", "1d3var"):
         dims = (int(rng.integers(1, 3000)),)
+    elif family == "3d7var":
+        dims = tuple(int(v) for v in rng.integers(1, 60, 3))
+    elif family == "3d7varbig":
+        # several 64 x 8 tiles, ragged edges, even nx (the TMA plane kernel)
+        dims = (2 * int(rng.integers(20, 90)), int(rng.integers(9, 70)),
+                int(rng.integers(1, 40)))
     elif family == "3d7":
         dims = tuple(int(v) for v in rng.integers(1, 70, 3))
     elif family == "3d7big":
@@ -49,13 +56,14 @@ def _case(family, seed):
 
 
 @pytest.mark.parametrize("seed", range(20))
-@pytest.mark.parametrize("family", ["1d3", "2d5", "2d5var", "3d7", "3d7big"])
+@pytest.mark.parametrize("family", ["1d3", "2d5", "2d5var", "3d7", "3d7big", "3d7var",
+                                    "3d7varbig", "1d3var"])
 def test_random_shape_cycle_bitwise(family, seed):
     import torch
 
     import paper_2011_06636_b200 as srj
     from oracle import srj_oracle as O
-    if family == "3d7big" and seed >= 8:
+    if family in ("3d7big", "3d7varbig") and seed >= 8:
         pytest.skip("8 seeds of the larger 3D grids")
     rng, dims = _case(family, seed)
     family = family.replace("big", "")
@@ -67,6 +75,17 @@ def test_random_shape_cycle_bitwise(family, seed):
         fy = rng.uniform(0.5, 30.0, (ny + 1, nx))
         make = lambda: srj.StencilOperator(family, dims, face_x=fx, face_y=fy, device=dev)
         op = O.StencilCPU(family, nx, ny, 1, 0.0, fx, fy)
+    elif family == "3d7var":
+        fx = rng.uniform(0.5, 30.0, (nz, ny, nx + 1))
+        fy = rng.uniform(0.5, 30.0, (nz, ny + 1, nx))
+        fz = rng.uniform(0.5, 30.0, (nz + 1, ny, nx))
+        make = lambda: srj.StencilOperator(family, dims, face_x=fx, face_y=fy, face_z=fz,
+                                           device=dev)
+        op = O.StencilCPU(family, nx, ny, nz, 0.0, fx, fy, fz)
+    elif family == "1d3var":
+        fx = rng.uniform(0.5, 30.0, nx + 1)
+        make = lambda: srj.StencilOperator(family, dims, face_x=fx, device=dev)
+        op = O.StencilCPU(family, nx, 1, 1, 0.0, fx)
     else:
         dx2 = float(rng.uniform(1.0, 50.0))
         make = lambda: srj.StencilOperator(family, dims, dx2=dx2, device=dev)

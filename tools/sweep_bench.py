@@ -25,11 +25,11 @@ def main():
     import paper_2011_06636_b200 as srj
     from paper_2011_06636_b200.solver import _OMEGAS
     dev = torch.device("cuda", 0)
-    bpu = {"1d3": 24, "2d5": 24, "3d7": 24, "2d5var": 40}
+    bpu = {"1d3": 24, "2d5": 24, "3d7": 24, "2d5var": 40, "3d7var": 48, "1d3var": 32}
     for spec in a.cases.split(","):
         fam, n = spec.split(":")
         n = int(n)
-        p = srj.baseline_problem(fam, n, seed=0, device=dev, rhs_on_device=(fam != "2d5var"))
+        p = srj.baseline_problem(fam, n, seed=0, device=dev, rhs_on_device=(fam in ("1d3", "2d5", "3d7")))
         A = p.A
         if a.spp > 0:
             A.set_sweeps_per_pass(a.spp)
