@@ -40,10 +40,14 @@ CONFIG_DESC = {
     "c1": "1D Poisson 3-pt N=1024 Dirichlet, f~U[-1,1) SplitMix64, rel L2 1e-8, SRJ heuristic",
     "c4": "2D var-coef 5-pt 4096^2 harmonic faces k=exp(g), rel L2 1e-8, SRJ heuristic",
     "c5": "3D Poisson 7-pt 1024x1024x(128N) z-slabs over N GPUs, 50 heuristic cycles",
+    "c3v": "3D var-coef 7-pt 512^3 harmonic faces k=exp(g), rel L2 1e-8, SRJ heuristic",
+    "c1v": "1D var-coef 3-pt N=1024 harmonic faces k=exp(g), rel L2 1e-8, SRJ heuristic",
 }
-BYTES_PER_UPDATE = {"1d3": 24, "2d5": 24, "3d7": 24, "2d5var": 40}
-# end-of-cycle residual pass: reads x and b (+ both face arrays, var-coef)
-RESIDUAL_BYTES = {"1d3": 16, "2d5": 16, "3d7": 16, "2d5var": 32}
+# x and b read, x written (+ the face arrays of the variable-coefficient
+# families: 2D east/north 2, 3D x/y/z 3, 1D 1; the diagonal is recomputed)
+BYTES_PER_UPDATE = {"1d3": 24, "2d5": 24, "3d7": 24, "2d5var": 40, "3d7var": 48, "1d3var": 32}
+# end-of-cycle residual pass: reads x and b (+ the face arrays, var-coef)
+RESIDUAL_BYTES = {"1d3": 16, "2d5": 16, "3d7": 16, "2d5var": 32, "3d7var": 40, "1d3var": 24}
 L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
 METRIC = {"default": "GLUP/s (SRJ point-updates/s); time-to-rel-residual 1e-8",
           "c5": "GLUP/s (SRJ point-updates/s), 50 heuristic cycles (throughput mode)"}
@@ -168,7 +172,8 @@ def traffic_from_profile(config):
     if not entry:
         return None
     return {"traffic": entry["traffic"], "alg_bytes": entry["alg_bytes"],
-            "ratio": entry["traffic_over_alg"], "launch": entry["launch"]}
+            "ratio": entry["traffic_over_alg"], "launch": entry["launch"],
+            "limiter": entry.get("limiter")}
 
 
 def kernel_name(family, info):
@@ -184,11 +189,16 @@ def cpu_sample(family, n, seed, budget_s):
     from oracle import srj_oracle as O
     # every host thread this process may run on (torchrun sets OMP_NUM_THREADS=1)
     O.clib().oracle_set_threads(len(os.sched_getaffinity(0)))
-    fx = fy = None
+    from paper_2011_06636_b200 import problems as pr
+    fx = fy = fz = None
+    dx2 = (n + 1.0) ** 2
     if family == "2d5var":
-        from paper_2011_06636_b200.problems import gaussian_field, harmonic_faces
-        fx, fy = harmonic_faces(np.exp(gaussian_field(n, seed)), (n + 1.0) ** 2)
-    op = O.stencil(family, n, fx=fx, fy=fy)
+        fx, fy = pr.harmonic_faces(np.exp(pr.gaussian_field(n, seed)), dx2)
+    elif family == "3d7var":
+        fx, fy, fz = pr.harmonic_faces_3d(np.exp(pr.gaussian_field_3d(n, seed)), dx2)
+    elif family == "1d3var":
+        fx = pr.harmonic_faces_1d(np.exp(pr.gaussian_field_1d(n, seed)), dx2)
+    op = O.stencil(family, n, fx=fx, fy=fy, fz=fz)
     b = O.uniform_rhs(seed, op.n)
     seq = O.scheme(O.LADDER[14])[0]
     x = np.zeros(op.n)
@@ -202,10 +212,104 @@ def cpu_sample(family, n, seed, budget_s):
         el = time.perf_counter() - t0
         if el >= budget_s:
             break
-    return {"value": op.n * sweeps / el / 1e9, "unit": "GLUP/s", "cores": O.clib().oracle_threads(),
-            "kind": "port", "seconds": el,
-            "sample": f"{sweeps} SRJ sweeps (update+residual+norm) of the {family} n={n} grid, "
-                      f"{el:.1f} s, oracle/srj_oracle.c OpenMP"}
+    out = {"value": op.n * sweeps / el / 1e9, "unit": "GLUP/s", "cores": O.clib().oracle_threads(),
+           "kind": "port", "seconds": el,
+           "sample": f"{sweeps} SRJ sweeps (update+residual+norm) of the {family} n={n} grid, "
+                     f"{el:.1f} s, oracle/srj_oracle.c OpenMP"}
+    out["host"] = host_info()
+    return out
+
+
+def host_info():
+    """What the CPU numbers were measured on."""
+    import platform
+
+    import numpy as np
+    info = {"nproc": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)),
+            "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS"),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS"),
+            "numpy": np.__version__, "python": platform.python_version()}
+    try:
+        import scipy
+        info["scipy"] = scipy.__version__
+    except Exception:
+        info["scipy"] = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    info["cpu_model"] = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return info
+
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_stock_sample(family, n, seed, budget_s):
+    """The UNMODIFIED reference (baseline/_ref, installed from /root/reference
+    with pip --target; pure Python + numpy/scipy) timed through its own public
+    `run_cycle` on a bounded sweep sample of the same grid: its CSR SparseMatrix
+    (from_coo, the path its solve takes), one level-14 scheme cycle cut by the
+    stopping rule's sweep budget.  Where the CSR does not fit (512^3 and up)
+    or baseline/_ref is absent, returns the reason instead."""
+    import numpy as np
+    if not os.path.isdir(os.path.join(REF_DIR, "srj")):
+        return {"unavailable": "baseline/_ref not installed"}
+    npts = n ** {"1d3": 1, "1d3var": 1, "2d5": 2, "2d5var": 2, "3d7": 3, "3d7var": 3}[family]
+    if npts > 20_000_000:
+        return {"unavailable": f"reference CSR for {npts} points does not fit host memory "
+                               "(SURVEY §8d: 512^3 needs a duck-typed operator)"}
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import srj as ref  # the reference package
+    from srj.sparse import SparseMatrix
+
+    from paper_2011_06636_b200.operators import StencilOperator
+    from paper_2011_06636_b200.problems import baseline_problem
+    # the reference's own CSR of the same operator (its constructor
+    # canonicalises and checks symmetry, as for a user matrix)
+    t_build = time.perf_counter()
+    if family in ("1d3", "3d7"):
+        gen = ref.poisson_1d if family == "1d3" else ref.poisson_3d
+        A = gen(n).A
+    else:
+        prob = baseline_problem(family, n, seed)
+        rows, cols, vals = prob.A.coo()
+        A = SparseMatrix.from_coo(npts, rows, cols, vals)
+    t_build = time.perf_counter() - t_build
+    from paper_2011_06636_b200.rng import uniform_rhs
+    b = uniform_rhs(seed, npts)
+    st = ref.SolverState(x=np.zeros(npts))
+    scheme = ref.scheme_for_level(14)
+    # whole level-14 cycles (the last one cut by the stopping rule's sweep
+    # budget) until the time budget is spent; one timed sweep sizes the cut
+    t0 = time.perf_counter()
+    ref.run_cycle(A, b, st, scheme, stopping=ref.StoppingRule("relative_l2", 1e-300, 1),
+                  baseline=1.0, record_history=False)
+    one = time.perf_counter() - t0
+    want = max(1, int(budget_s / max(one, 1e-9)))
+    done, cycles = 0, 0
+    t0 = time.perf_counter()
+    while done < want:
+        k = min(scheme.M, want - done)
+        st, stats = ref.run_cycle(A, b, st, scheme,
+                                  stopping=ref.StoppingRule("relative_l2", 1e-300,
+                                                            st.total_iterations + k),
+                                  baseline=1.0, record_history=False)
+        done += stats.executed
+        cycles += 1
+    el = time.perf_counter() - t0
+    stats = type("S", (), {"executed": done})
+    del StencilOperator
+    return {"value": npts * stats.executed / el / 1e9, "unit": "GLUP/s", "cores": 1,
+            "kind": "reference",
+            "sample": f"{stats.executed} sweeps in {cycles} level-14 run_cycle calls of the stock "
+                      f"reference (baseline/_ref, CSR of {npts} points, built in {t_build:.1f} s), "
+                      f"{el:.1f} s; scipy csr_matvec is single-threaded",
+            "seconds": el}
 
 
 def run_reference(args, rank, world):
@@ -226,7 +330,7 @@ def run_reference(args, rank, world):
         vals.append(c["value"])
         samples.append(c)
     v = sum(vals) / len(vals)
-    npts = {"1d3": n, "2d5": n * n, "2d5var": n * n, "3d7": n ** 3}[family]
+    npts = n ** {"1d3": 1, "1d3var": 1, "2d5": 2, "2d5var": 2, "3d7": 3, "3d7var": 3}[family]
     line = {
         "impl": "reference", "metric": METRIC.get(args.config, METRIC["default"]), "value": v,
         "unit": "GLUP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -236,7 +340,10 @@ def run_reference(args, rank, world):
         "dtype": "f64", "data": "synthetic (SplitMix64 f, seeded)",
         "config": {"workload": CONFIG_DESC[args.config], "n": npts, "grid": n},
         "cpu_baseline": {"value": v, "unit": "GLUP/s", "cores": samples[-1]["cores"],
-                         "kind": "port", "sample": samples[-1]["sample"]},
+                         "kind": "port", "sample": samples[-1]["sample"],
+                         "host": samples[-1].get("host"),
+                         "reference_stock": reference_stock_sample(family, n, args.seed,
+                                                                   min(args.cpu_seconds, 10.0))},
         "e2e": {"value": v, "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -548,6 +655,21 @@ def run_ours(args, rank, world, local):
         e2e_total = float(t.item())
     e2e_val = A.n * sum(e2e_sweeps) * world / (e2e_total * 1e-3) / 1e9
 
+    # north_star's host-side scheme selection: the same solve with the
+    # controller loop on the host (one launch + one small D2H per cycle)
+    host_loop_ms = None
+    if not args.host_loop and A.solve_supported():
+        flush.fill_(1.0)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        x.buf.zero_()
+        r3 = solve_fields(A, b, x, x_alt, ctrl, rule, record_history=False, device_loop=False)
+        e1.record(stream)
+        e1.synchronize()
+        host_loop_ms = e0.elapsed_time(e1)
+        assert r3.total_iterations == rep.total_iterations
+
     info = A.describe()
     peak, peak_kind = measured_peak()
     achieved = sum(launch_bytes) / (sum(launch_ms) * 1e-3) / 1e9 if launch_ms else None
@@ -563,6 +685,10 @@ def run_ours(args, rank, world, local):
                    "levels": [c.level for c in rep.cycles],
                    "executed": [c.executed for c in rep.cycles],
                    "time_to_tolerance_ms": ms_per_step,
+                   "time_to_tolerance_ms_host_loop": host_loop_ms,
+                   "controller": "device-resident loop (srj_solve)" if (
+                       A.solve_supported() and not args.host_loop) else "host loop",
+                   "margins": margins(rep.cycles, args.tol),
                    "l2": "flushed between steps (512 MiB write)",
                    "sweeps_per_pass": info["sweeps_per_pass"] if info["tb_supported"] else 1,
                    "launch": info,
@@ -578,16 +704,49 @@ def run_ours(args, rank, world, local):
                      "traffic_launch": traffic["launch"] if traffic else None,
                      "peak_kind": peak_kind, "kernel": kernel_name(family, info),
                      "bytes_per_update": bpu,
-                     "launches_timed": len(launch_ms)},
+                     "launches_timed": len(launch_ms),
+                     **dram_view(achieved, peak, traffic)},
         "clocks": clocks.summary(),
         "gpu_launches": launches,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # N = 1 only (contract)
         line["cpu_baseline"] = cpu_sample(family, n, args.seed, args.cpu_seconds)
+        line["cpu_baseline"]["reference_stock"] = reference_stock_sample(
+            family, n, args.seed, min(args.cpu_seconds, 10.0))
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def margins(cycles, tol):
+    """How far this solve is from a different scheme sequence or sweep count:
+    the smallest |ratio - 0.4| and |ratio - 0.2| over the cycles (Heuristic
+    thresholds, solver.py:125-140) and the last residual's distance below tol."""
+    r = [c.residual_after / c.residual_before for c in cycles
+         if c.residual_before > 0 and c.residual_after > 0]
+    if not r:
+        return None
+    return {"min_abs_ratio_minus_0.4": min(abs(v - 0.4) for v in r),
+            "min_abs_ratio_minus_0.2": min(abs(v - 0.2) for v in r),
+            "last_res_after_over_tol": cycles[-1].residual_after / tol}
+
+
+def dram_view(achieved, peak, traffic):
+    """The roofline block's `achieved` is ALGORITHMIC bytes / kernel time (the
+    contract's definition).  With temporal blocking and L2 residency that is an
+    effective bandwidth above the HBM peak; the DRAM bandwidth the kernel really
+    drew is achieved x traffic_over_alg (ncu DRAM bytes of a captured launch /
+    its algorithmic bytes), and the limiter comes from that capture's stall
+    profile (profiles/traffic.json)."""
+    if not achieved or not traffic:
+        return {}
+    dram = achieved * traffic["ratio"]
+    out = {"achieved_is": "effective (algorithmic bytes / time)",
+           "dram_achieved": dram, "dram_frac": dram / peak}
+    if traffic.get("limiter"):
+        out["limiter"] = traffic["limiter"]
+    return out
 
 
 def main():

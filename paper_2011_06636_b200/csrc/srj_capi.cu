@@ -239,21 +239,30 @@ constexpr int kReg1dWarps = 8;      // most warps (n <= 32 * 8 * 16 = 4096)
 constexpr int kReg1dBatch = 32;     // sweeps per stop-test batch (16 for P = 16: registers)
 
 // The register kernel applies c_diag*x as -2*p (exact: c_diag = -2 c_off).
+// VAR keeps faces and 1/diag per point in registers as well: at most 8
+// points per lane (n <= 2048; 16 per lane spill several KB).
 static bool reg1d_ok(const Geom& g) {
-    return g.fam == F1D && g.nx <= 32 * kReg1dWarps * 16 && g.c_diag == -2.0 * g.c_off;
+    return (g.fam == F1D && g.nx <= 32 * kReg1dWarps * 16 && g.c_diag == -2.0 * g.c_off) ||
+           (g.fam == F1DV && g.nx <= 32 * kReg1dWarps * 8);
 }
 
 // Warps of the register kernel for n points: 4 up to 2048 (one barrier among
 // fewer warps is cheaper: C1 3.56 -> 3.40 ms), else 8; points per lane P.
-static void reg1d_shape(int n, int& nw, int& per) {
-    nw = n <= 32 * 4 * 16 ? 4 : 8;
+static void reg1d_shape(int n, int& nw, int& per, bool var = false) {
+    nw = n <= 32 * 4 * (var ? 8 : 16) ? 4 : 8;
     per = (n + 32 * nw - 1) / (32 * nw);
     per = per <= 2 ? 2 : per <= 4 ? 4 : per <= 8 ? 8 : 16;
 }
 
-template <int NW, int P, bool FULL, bool SOLVE>
+//
+// VAR (SRJ_STENCIL_1D3_VAR): per point the faces c_w, c_e, the diagonal
+// d = c_w + c_e and 1/d (the reference's division) stay in registers; no
+// product is shared between neighbours (each face multiplies two different
+// x), so x itself crosses lanes and warps and
+// y = ((0 + (-c_w) x_w) + d x) + (-c_e) x_e in the reference's order.
+template <int NW, int P, bool FULL, bool SOLVE, bool VAR>
 __global__ void __launch_bounds__(32 * NW) k_reg_cycle_1d(CycleArgs a) {
-    constexpr int K = P <= 8 ? kReg1dBatch : 16;
+    constexpr int K = (P <= 8 && !(VAR && P == 8)) ? kReg1dBatch : 16;
     __shared__ double edge[2][2][NW + 2];  // [parity][first|last][warp + 1]
     __shared__ double red[K][NW + 1];
     __shared__ double stop_sum;
@@ -262,15 +271,39 @@ __global__ void __launch_bounds__(32 * NW) k_reg_cycle_1d(CycleArgs a) {
     const double c = a.g.c_off, inv = a.g.inv_diag;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int i0 = (wid * 32 + lane) * P;
-    double x[P], b[P], p[P], xs[P];
+    double x[P], b[P], p_[P], xs[P];
+    // the neighbours' view: p = c*x (shared products), or x itself (VAR)
+    double (&p)[P] = VAR ? x : p_;
+    // VAR: west faces, the lane's last east face and 1/diagonal per point
+    double fw[VAR ? P : 1], iv[VAR ? P : 1], fel = 0.0;
+    // the value a neighbour needs: p = c*x (shared product) or x itself (VAR)
+    auto pv = [&](double xv) __attribute__((always_inline)) -> double {
+        if constexpr (VAR) return xv;
+        else return DMUL(c, xv);
+    };
 #pragma unroll
     for (int j = 0; j < P; ++j) {
         const bool in = FULL || i0 + j < n;
         x[j] = in ? a.xa[i0 + j] : 0.0;
         b[j] = in ? a.b[i0 + j] : 0.0;
-        p[j] = DMUL(c, x[j]);
+        p[j] = pv(x[j]);
+        if constexpr (VAR) {
+            fw[j] = in ? __ldg(a.g.fx + i0 + j) : 0.0;
+            if (j == P - 1) fel = in ? __ldg(a.g.fx + i0 + j + 1) : 0.0;
+        }
     }
-    const double pz = DMUL(c, 0.0);  // ghost / past-n neighbour: c*0 (a no-op term)
+    // east face of point j = west face of j+1; diag = c_w + c_e
+    auto fe = [&](int j) __attribute__((always_inline)) -> double {
+        return j == P - 1 ? fel : fw[j + 1];
+    };
+    if constexpr (VAR) {
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            const bool in = FULL || i0 + j < n;
+            iv[j] = in ? __drcp_rn(DADD(fw[j], fe(j))) : 0.0;  // sparse.py:42-44 (1.0 / diag)
+        }
+    }
+    const double pz = pv(0.0);  // ghost / past-n neighbour: c*0 or 0 (a no-op term)
     if (threadIdx.x < 2 * 2 * (NW + 2)) (&edge[0][0][0])[threadIdx.x] = pz;
     __syncthreads();
     if (lane == 0) edge[0][0][wid + 1] = p[0];
@@ -293,17 +326,24 @@ __global__ void __launch_bounds__(32 * NW) k_reg_cycle_1d(CycleArgs a) {
         double r[P], acc = 0.0;
 #pragma unroll
         for (int j = 0; j < P; ++j) {
-            double y = __fma_rn(p[j], -2.0, j == 0 ? pl : p[j - 1]);
-            y = DADD(y, j == P - 1 ? pr : p[j + 1]);
+            double y;
+            if constexpr (VAR) {
+                y = DADD(0.0, DMUL(-fw[j], j == 0 ? pl : p[j - 1]));
+                y = DADD(y, DMUL(DADD(fw[j], fe(j)), x[j]));
+                y = DADD(y, DMUL(-fe(j), j == P - 1 ? pr : p[j + 1]));
+            } else {
+                y = __fma_rn(p[j], -2.0, j == 0 ? pl : p[j - 1]);
+                y = DADD(y, j == P - 1 ? pr : p[j + 1]);
+            }
             r[j] = DSUB(b[j], y);
             if (FULL || i0 + j < n) acc = fma(r[j], r[j], acc);
         }
         if (update) {
 #pragma unroll
             for (int j = 0; j < P; ++j) {
-                const double xn = relax(x[j], inv, r[j], w);
+                const double xn = relax(x[j], VAR ? iv[j] : inv, r[j], w);
                 x[j] = (FULL || i0 + j < n) ? xn : 0.0;
-                p[j] = DMUL(c, x[j]);
+                if constexpr (!VAR) p[j] = pv(x[j]);
             }
             // one predicated store (lanes 0 and 31), no divergent branch
             if (lane == 0 || lane == 31)
@@ -400,7 +440,7 @@ __global__ void __launch_bounds__(32 * NW) k_reg_cycle_1d(CycleArgs a) {
 #pragma unroll
                     for (int j = 0; j < P; ++j) {
                         x[j] = xs[j];
-                        p[j] = DMUL(c, x[j]);
+                        if constexpr (!VAR) p[j] = pv(x[j]);
                     }
                     if (lane == 0) edge[par][0][wid + 1] = p[0];
                     if (lane == 31) edge[par][1][wid + 1] = p[P - 1];
@@ -493,20 +533,27 @@ __global__ void __launch_bounds__(32 * NW) k_reg_cycle_1d(CycleArgs a) {
     }
 }
 
-template <bool SOLVE>
-static void reg1d_launch(int nw, int per, bool full, const CycleArgs& a, cudaStream_t st) {
-#define SRJ_REG1D(NWW, PP)                                                         \
-    if (full) k_reg_cycle_1d<NWW, PP, true, SOLVE><<<1, 32 * NWW, 0, st>>>(a);    \
-    else k_reg_cycle_1d<NWW, PP, false, SOLVE><<<1, 32 * NWW, 0, st>>>(a)
+template <bool SOLVE, bool VAR>
+static void reg1d_launch_v(int nw, int per, bool full, const CycleArgs& a, cudaStream_t st) {
+#define SRJ_REG1D(NWW, PP)                                                               \
+    if (full) k_reg_cycle_1d<NWW, PP, true, SOLVE, VAR><<<1, 32 * NWW, 0, st>>>(a);     \
+    else k_reg_cycle_1d<NWW, PP, false, SOLVE, VAR><<<1, 32 * NWW, 0, st>>>(a)
     if (nw == 4) {
         if (per == 2) { SRJ_REG1D(4, 2); }
         else if (per == 4) { SRJ_REG1D(4, 4); }
         else if (per == 8) { SRJ_REG1D(4, 8); }
-        else { SRJ_REG1D(4, 16); }
+        else if constexpr (!VAR) { SRJ_REG1D(4, 16); }
     } else {
-        SRJ_REG1D(8, 16);
+        if constexpr (VAR) { SRJ_REG1D(8, 8); }
+        else { SRJ_REG1D(8, 16); }
     }
 #undef SRJ_REG1D
+}
+
+template <bool SOLVE>
+static void reg1d_launch(int nw, int per, bool full, const CycleArgs& a, cudaStream_t st) {
+    if (a.g.fam == F1DV) reg1d_launch_v<SOLVE, true>(nw, per, full, a, st);
+    else reg1d_launch_v<SOLVE, false>(nw, per, full, a, st);
 }
 
 template <int FAM, int MODE>
@@ -890,7 +937,7 @@ static int launch_cycle(srj_op* op, const double* xa, double* xb, const double* 
     a.out_d = op->out_d;
     if (!diff && reg1d_ok(op->g)) {
         int nw, per;
-        reg1d_shape(op->g.nx, nw, per);
+        reg1d_shape(op->g.nx, nw, per, op->g.fam == F1DV);
         const bool full = op->g.nx == per * 32 * nw;
         reg1d_launch<false>(nw, per, full, a, st);
         CUDA_TRY(cudaGetLastError());
@@ -1084,7 +1131,7 @@ int srj_solve(srj_op* op, double* x, double* x_alt, const double* b, const srj_s
         a.out_d = op->out_d;
         a.ctl = c;
         int nw, per;
-        reg1d_shape(g.nx, nw, per);
+        reg1d_shape(g.nx, nw, per, g.fam == F1DV);
         reg1d_launch<true>(nw, per, g.nx == per * 32 * nw, a, st);
         CUDA_TRY(cudaGetLastError());
     } else if (kern == SRJ_KERNEL_TBVAR)

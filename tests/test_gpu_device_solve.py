@@ -20,7 +20,8 @@ pytestmark = pytest.mark.gpu
 
 CASES = ["c1_seed0", "poisson1d_100_heuristic", "poisson1d_100_increasing", "fixed5_tol_tiny",
          "increasing_clamp", "tiny_1d_n1", "c2_32", "c2_64", "c3_16", "c4_32",
-         "budget_midcycle_2d", "fixed2362_3d", "poisson3d_24_ones"]
+         "budget_midcycle_2d", "fixed2362_3d", "poisson3d_24_ones", "c1v_1024", "c1v_100_s2",
+         "c3v_12"]
 
 
 def _solve(c, device_loop, record_history=True, spp=None):
@@ -29,12 +30,8 @@ def _solve(c, device_loop, record_history=True, spp=None):
     import paper_2011_06636_b200 as srj
     from paper_2011_06636_b200.solver import solve_fields
     dev = torch.device("cuda", 0)
-    fam, n, b, fx, fy = P.case_inputs(c)
-    dims = {"1d3": (n,), "2d5": (n, n), "2d5var": (n, n), "3d7": (n, n, n)}[fam]
-    if fam == "2d5var":
-        A = srj.StencilOperator(fam, dims, face_x=fx, face_y=fy, device=dev)
-    else:
-        A = srj.StencilOperator(fam, dims, device=dev)
+    fam, n, b, _, _ = P.case_inputs(c)
+    A = P.case_operator(c, device=dev)
     if spp:
         A.set_sweeps_per_pass(spp)
     ctrl = c["controller"]
