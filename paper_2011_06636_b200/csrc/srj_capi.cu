@@ -288,8 +288,10 @@ __global__ void __launch_bounds__(32 * NW) k_reg_cycle_1d(CycleArgs a) {
         b[j] = in ? a.b[i0 + j] : 0.0;
         p[j] = pv(x[j]);
         if constexpr (VAR) {
-            fw[j] = in ? __ldg(a.g.fx + i0 + j) : 0.0;
-            if (j == P - 1) fel = in ? __ldg(a.g.fx + i0 + j + 1) : 0.0;
+            // faces 0..n exist: the point past the last one still carries the
+            // last point's east (boundary) face
+            fw[j] = (FULL || i0 + j <= n) ? __ldg(a.g.fx + i0 + j) : 0.0;
+            if (j == P - 1) fel = (FULL || i0 + j + 1 <= n) ? __ldg(a.g.fx + i0 + j + 1) : 0.0;
         }
     }
     // east face of point j = west face of j+1; diag = c_w + c_e
