@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(32 * NW) k_reg_cycle_1d(CycleArgs a) {
     // the neighbours' view: p = c*x (shared products), or x itself (VAR)
     double (&p)[P] = VAR ? x : p_;
     // VAR: west faces, the lane's last east face and 1/diagonal per point
-    double fw[VAR ? P : 1], iv[VAR ? P : 1], fel = 0.0;
+    double fw[P], iv[VAR ? P : 1], fel = 0.0;
     // the value a neighbour needs: p = c*x (shared product) or x itself (VAR)
     auto pv = [&](double xv) __attribute__((always_inline)) -> double {
         if constexpr (VAR) return xv;
