@@ -1216,6 +1216,10 @@ int srj_tb_pass(srj_op* op, double* x, double* x_alt, const double* b,
     const bool is3d = op->tb3.supported;
     if (h < 1 || h > (is3d ? op->tb3.sweeps : kTbPassMax))
         return fail(SRJ_BAD_ARGUMENT, "sweeps per pass out of range");
+    // a pass must not fuse more sweeps than the selected ring holds (the
+    // SRJ_TB_VARIANT tuning override can pin the S = 4 ring)
+    if (!is3d && !op->tbv.supported && h > tb_ring_for(op->tb, h))
+        return fail(SRJ_BAD_ARGUMENT, "sweeps per pass exceed the selected ring width");
     if (row_lo < 0 || row_lo >= row_hi || row_hi > (is3d ? op->g.nz : op->g.ny))
         return fail(SRJ_BAD_ARGUMENT, "owned rows out of range");
     DeviceGuard guard(op->device);

@@ -524,6 +524,10 @@ int tb_variant_for(const TbPlan& plan, int s) {
     return s > tb2d::Cfg<0>::S ? 1 : 0;
 }
 
+int tb_ring_for(const TbPlan& plan, int s) {
+    return tb_variant_for(plan, s) == 1 ? tb2d::Cfg<1>::S : tb2d::Cfg<0>::S;
+}
+
 cudaError_t tb_plan_init(TbPlan& plan, const Geom& g, int num_sms) {
     plan = TbPlan();
     // TMA needs 16-byte row pitch: even nx.

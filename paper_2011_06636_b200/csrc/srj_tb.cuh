@@ -26,6 +26,8 @@ cudaError_t tb_plan_init(TbPlan& plan, const Geom& g, int num_sms);
 // Kernel variant (tb2d::Cfg<K>) serving s sweeps per pass: K=0 (S=4 ring)
 // for s <= 4, K=1 (S=6 ring) for s = 5, 6.
 int tb_variant_for(const TbPlan& plan, int s);
+// Sweeps one pass of the variant chosen for s can fuse (its ring width S).
+int tb_ring_for(const TbPlan& plan, int s);
 
 // ctl != nullptr (all three TB launchers): a device-resident solve from x
 // (srj_tbdriver.cuh tb_run_solve) instead of one cycle; M and omegas are then

@@ -498,6 +498,7 @@ class TbSlab:
         self.row0 = r0
         self.x = self.A.new_field()
         self.x_alt = self.A.new_field()
+        self.pair = (self.x, self.x_alt)  # fixed identities (CUDA-graph keys)
         self.snap = self.A.new_field()
         self.b = self.A.new_field()
 
@@ -526,6 +527,8 @@ class TbSlab:
 class LocalTbExchanger(LocalExchanger):
     """Virtual ranks in one process: deep ghost rows by device copies."""
 
+    graph_capturable = True
+
     def start_rows(self, slabs, fields):
         g = slabs[0].ghost
         for lo, hi, flo, fhi in zip(slabs[:-1], slabs[1:], fields[:-1], fields[1:]):
@@ -538,6 +541,10 @@ class LocalTbExchanger(LocalExchanger):
 
 class TorchTbExchanger(TorchExchanger):
     """One slab per process: deep ghost rows over torch.distributed P2P."""
+
+    # NCCL P2P inside CUDA-graph capture is not exercised here (one GPU per
+    # call): opt in with TbSlabSolver(graphs=True)
+    graph_capturable = False
 
     def start_rows(self, slabs, fields):
         (s,), (f,) = slabs, fields
@@ -568,8 +575,19 @@ class TbSlabSolver(SlabSolver):
     once it has arrived.  Iterates are identical either way; the per-sweep sums
     are added interior + lower + upper (fixed order)."""
 
-    def __init__(self, slabs: list[TbSlab], exchanger, overlap: bool | None = None):
+    def __init__(self, slabs: list[TbSlab], exchanger, overlap: bool | None = None,
+                 graphs: bool | None = None):
         super().__init__(slabs, exchanger, engine=None)
+        # graphs (None: where the exchanger is capturable): the forward part of
+        # a cycle -- snapshot, every pass with its exchange, the residual of
+        # x_M -- is captured once per (sweeps, scheme, buffer parity) into a
+        # CUDA graph and replayed: one graph launch per cycle instead of
+        # ~M/ghost rounds of host work (tensor-map encodes, cooperative
+        # launches, exchange calls)
+        self.graphs = (getattr(exchanger, "graph_capturable", False) if graphs is None
+                       else bool(graphs))
+        self._graph_cache = {}
+        self._graph_seen = set()
         g = slabs[0].ghost
         if any(s.count < g for s in slabs):
             raise ValueError(f"every slab needs at least {g} rows")
@@ -705,11 +723,7 @@ class TbSlabSolver(SlabSolver):
         if Meff == 0:
             return 0, "ran", res_before, []
         om = self._omegas(ordered_omegas)
-        for s in self.slabs:
-            s.snap.buf.copy_(s.x.buf)
-        sums = self._sums_buffer(Meff + 1)
-        self._passes(om, sums, Meff)
-        self._residual_into(sums, Meff)
+        sums = self._forward(om, Meff)
         res = np.sqrt(self._global(sums, Meff + 1)) / baseline
         stop, status = None, "ran"
         for k in range(1, Meff + 1):
@@ -726,6 +740,52 @@ class TbSlabSolver(SlabSolver):
                 s.x.buf.copy_(s.snap.buf)
             self._passes(om, self._sums_buffer(Meff + 1), executed)
         return executed, status, float(res[executed]), [float(v) for v in res[1:executed + 1]]
+
+    def _forward_eager(self, om, Meff: int, sums) -> None:
+        for s in self.slabs:
+            s.snap.buf.copy_(s.x.buf)
+        for sm in sums:
+            sm.zero_()
+        self._passes(om, sums, Meff)
+        self._residual_into(sums, Meff)
+
+    def _forward(self, om, Meff: int):
+        """Snapshot, Meff sweeps in passes, residual of x_Meff; returns the
+        per-slab per-sweep sums (device).  Graph mode: the first cycle of a
+        key runs eagerly (it also creates every handle and workspace), the
+        second captures, later ones replay."""
+        if not self.graphs:
+            sums = self._sums_buffer(Meff + 1)
+            self._forward_eager(om, Meff, sums)
+            return sums
+        torch = _torch()
+        parity = tuple(s.x is s.pair[0] for s in self.slabs)
+        key = (Meff, om.data_ptr(), parity)
+        hit = self._graph_cache.get(key)
+        if hit is None and key not in self._graph_seen:
+            self._graph_seen.add(key)
+            sums = self._sums_buffer(Meff + 1)
+            self._forward_eager(om, Meff, sums)
+            return sums
+        if hit is None:
+            sums = self._sums_buffer(Meff + 1)
+            launches0 = self.launches
+            g = torch.cuda.CUDAGraph()
+            dev = self.slabs[0].x.buf.device
+            torch.cuda.synchronize(dev)
+            with torch.cuda.graph(g):
+                self._forward_eager(om, Meff, sums)
+            end = tuple(s.x is s.pair[0] for s in self.slabs)
+            hit = self._graph_cache[key] = (g, sums, end, self.launches - launches0)
+            # capture recorded the work and moved the Python-side buffer roles
+            # exactly as an execution would; now run it
+            self.launches = launches0
+        g, sums, end, nl = hit
+        g.replay()
+        for s, e in zip(self.slabs, end):
+            s.x, s.x_alt = (s.pair[0], s.pair[1]) if e else (s.pair[1], s.pair[0])
+        self.launches += nl
+        return sums
 
     def solve(self, *args, **kwargs) -> SolveReport:
         rep = super().solve(*args, **kwargs)

@@ -410,8 +410,7 @@ class StencilOperator(DeviceOperator):
     @property
     def planes(self) -> int:
         """Planes along the slab axis (z in 3D, rows in 2D, 1 in 1D)."""
-        return {"1d3": 1, "1d3var": 1, "2d5": self.shape[1], "2d5var": self.shape[1],
-                "3d7": self.shape[2], "3d7var": self.shape[2]}[self.family]
+        return 1 if DIMS[self.family] == 1 else self.shape[-1]
 
     # ------------------------------------------------------------ device side
     def _fill_desc(self, desc, dev) -> None:

@@ -178,3 +178,46 @@ def test_tb_slabs_with_reserved_sms(name):
     rule = srj.StoppingRule(c["norm"], c["tol"], c.get("max_iterations", 10**9))
     rep = solver.solve(srj.Heuristic(), rule, record_history=False)
     P.assert_trace_matches(c, _rows(rep), rep.total_iterations, rep.converged, x=solver.gather())
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+@pytest.mark.parametrize("name,world", [("c2_64", 3), ("c4_64", 2), ("c3_32", 3)])
+def test_tb_slabs_graph_replay_matches_reference(name, world, graphs):
+    """The cycle's forward work captured in a CUDA graph and replayed (the
+    default with virtual ranks) gives the reference's trace and iterate, and
+    so does the eager path."""
+    import torch
+
+    import paper_2011_06636_b200 as srj
+    from paper_2011_06636_b200.distributed import (LocalTbExchanger, TbSlabSolver,
+                                                   local_tb_slabs)
+    c = P.case(name)
+    fam, n, b, fx, fy = P.case_inputs(c)
+    shape = (n, n, n) if fam == "3d7" else (n, n)
+    slabs = local_tb_slabs(fam, shape, world, range(world), torch.device("cuda", 0),
+                           face_x=fx, face_y=fy)
+    solver = TbSlabSolver(slabs, LocalTbExchanger(world), graphs=graphs)
+    solver.load(b=b)
+    rule = srj.StoppingRule(c["norm"], c["tol"], c.get("max_iterations", 10**9))
+    rep = solver.solve(srj.Heuristic(), rule, record_history=False)
+    P.assert_trace_matches(c, _rows(rep), rep.total_iterations, rep.converged, x=solver.gather())
+    if graphs:
+        assert solver._graph_cache, "no cycle was replayed from a graph"
+
+
+def test_tb_pass_rejects_more_sweeps_than_the_ring(monkeypatch):
+    """SRJ_TB_VARIANT=0 pins the S = 4 ring: a 6-sweep srj_tb_pass must fail
+    (bad argument) instead of silently running 4 sweeps (advisor finding)."""
+    import torch
+
+    import paper_2011_06636_b200 as srj
+    from paper_2011_06636_b200._lib import SrjLibraryError
+    monkeypatch.setenv("SRJ_TB_VARIANT", "0")
+    dev = torch.device("cuda", 0)
+    A = srj.StencilOperator("2d5", (64, 40), device=dev)
+    x, xa, b = A.new_field(), A.new_field(), A.new_field()
+    om = torch.ones(6, dtype=torch.float64, device=dev)
+    sums = torch.zeros(6, dtype=torch.float64, device=dev)
+    with pytest.raises(SrjLibraryError):
+        A.tb_pass(x, xa, b, om.data_ptr(), 6, 0, 40, sums.data_ptr())
+    A.tb_pass(x, xa, b, om.data_ptr(), 4, 0, 40, sums.data_ptr())  # within the ring: fine
