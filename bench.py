@@ -75,6 +75,10 @@ def parse():
                          "the device-resident solve exists")
     ap.add_argument("--no-tb-slabs", action="store_true",
                     help="slabs: one sweep per launch instead of temporally blocked passes")
+    ap.add_argument("--exchange", default="torch", choices=["torch", "native"],
+                    help="slabs at N > 1: deep-halo exchange over torch.distributed P2P, or "
+                         "libsrj's own NCCL communicator with one srj_slab_cycle_forward call "
+                         "per cycle (no exchange/compute split)")
     return ap.parse_args()
 
 
@@ -396,7 +400,11 @@ def run_slabs(args, rank, world, local):
           and shape[-1] // world >= tb_ghost(family) and not args.no_tb_slabs)
     if tb:
         slabs = local_tb_slabs(family, shape, world, [rank], dev, face_x=face_x, face_y=face_y)
-        solver = TbSlabSolver(slabs, TorchTbExchanger() if world > 1 else LocalTbExchanger(1))
+        if world > 1 and args.exchange == "native":
+            from paper_2011_06636_b200.distributed import NcclTbExchanger
+            solver = TbSlabSolver(slabs, NcclTbExchanger(dev), overlap=False)
+        else:
+            solver = TbSlabSolver(slabs, TorchTbExchanger() if world > 1 else LocalTbExchanger(1))
     else:
         slabs = local_slabs(family, shape, world, [rank], dev, face_x=face_x, face_y=face_y)
         solver = SlabSolver(slabs, TorchExchanger() if world > 1 else LocalExchanger(1))

@@ -307,6 +307,49 @@ int srj_matvec(srj_op* op, const double* x, double* y, void* stream);
 int srj_fill_uniform_rhs(double* out, int64_t n, uint64_t seed, int64_t start,
                          int32_t device, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Multi-GPU: one NCCL communicator per device.
+ * The reference has no multi-process solve (its only concurrency is a process
+ * pool of independent solves, cli.py:196-198); these entry points replace the
+ * Python-side exchange of distributed.py (TorchTbExchanger) with native,
+ * stream-ordered NCCL calls.  NCCL is loaded at run time (libnccl.so.2).
+ * ------------------------------------------------------------------------- */
+#define SRJ_NCCL_ID_BYTES 128
+int srj_nccl_available(void);                       /* 1 if libnccl.so.2 resolved */
+const char* srj_nccl_last_error(void);
+int srj_nccl_unique_id(uint8_t id[SRJ_NCCL_ID_BYTES]);   /* on one rank, then broadcast */
+int srj_nccl_comm_init(int32_t nranks, const uint8_t id[SRJ_NCCL_ID_BYTES], int32_t rank,
+                       int32_t device, void** comm);
+int srj_nccl_comm_destroy(void* comm);
+/* Deep-halo exchange of a temporally blocked slab operator whose planes are
+ * [0, g_lo) ghost, [g_lo, g_lo+count) owned, [g_lo+count, +g_hi) ghost: the
+ * first / last `rows` owned planes go to rank-1 / rank+1 and their boundary
+ * planes arrive in this slab's ghost planes, one NCCL group on `stream`. */
+int srj_slab_exchange(const srj_op* op, void* comm, int32_t rank, int32_t nranks, double* x,
+                      int64_t g_lo, int64_t count, int64_t g_hi, int32_t rows, void* stream);
+/* The exchange's element offsets from x (first interior point) for planes of
+ * `unit` points: plan[0] sent to rank-1, plan[1] received from rank-1,
+ * plan[2] sent to rank+1, plan[3] received from rank+1, plan[4] values per
+ * message.  No CUDA call.  The in-process virtual-rank exchanger copies by the
+ * same plan, so every slab test exercises it. */
+int srj_slab_exchange_plan(int64_t unit, int32_t rank, int32_t nranks, int64_t g_lo,
+                           int64_t count, int64_t g_hi, int32_t rows, int64_t plan[5]);
+/* gathered[r*K + k] = rank r's sums[k] (ncclAllGather; a copy when nranks == 1). */
+int srj_allgather_sums(void* comm, int32_t nranks, const double* sums, double* gathered,
+                       int64_t K, void* stream);
+/* The forward part of one slab cycle (distributed.py TbSlabSolver.cycle):
+ * snapshot x into x_snap (optional), M sweeps in passes of <= `ghost` sweeps
+ * (each: exchange + srj_tb_pass over the owned planes), the exchange and
+ * residual of x_M (sums_dev[M]), and the all-gather of the M+1 per-sweep owned
+ * sums into gathered_dev[nranks*(M+1)].  No host synchronisation; x_M is in
+ * x_alt when *result_in_alt.  The host applies the stopping rule to the rank-
+ * ordered sums and rolls back from x_snap when a sweep inside stops. */
+int srj_slab_cycle_forward(srj_op* op, void* comm, int32_t rank, int32_t nranks, double* x,
+                           double* x_alt, double* x_snap, const double* b,
+                           const double* omegas_dev, int32_t M, int32_t ghost, int64_t g_lo,
+                           int64_t count, int64_t g_hi, double* sums_dev, double* gathered_dev,
+                           int32_t* result_in_alt, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,6 +30,9 @@ EXPORTED_SYMBOLS = (
     "srj_op_planes", "srj_sweep_planes", "srj_run_cycle_diffinf", "srj_batch_cycles_1d",
     "srj_op_set_temporal_kernel", "srj_tb_pass", "srj_op_solve_supported", "srj_solve",
     "srj_op_set_reserved_sms",
+    "srj_nccl_available", "srj_nccl_last_error", "srj_nccl_unique_id", "srj_nccl_comm_init",
+    "srj_nccl_comm_destroy", "srj_slab_exchange", "srj_allgather_sums", "srj_slab_cycle_forward",
+    "srj_slab_exchange_plan",
 )
 SOLVE_PAUSED, SOLVE_CONVERGED, SOLVE_DIVERGED, SOLVE_BUDGET = 0, 1, 2, 3
 SOLVE_HEURISTIC, SOLVE_INCREASING, SOLVE_FIXED = 0, 1, 2
@@ -137,8 +140,21 @@ def _declare(L):
     L.srj_op_set_reserved_sms.argtypes = [c_void_p, c_int32]
     L.srj_solve.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, POINTER(SolveArgs), c_double,
                             c_double, c_void_p, c_void_p, POINTER(SolveOut), c_void_p]
+    L.srj_nccl_last_error.restype = ctypes.c_char_p
+    L.srj_nccl_unique_id.argtypes = [c_void_p]
+    L.srj_nccl_comm_init.argtypes = [c_int32, c_void_p, c_int32, c_int32, POINTER(c_void_p)]
+    L.srj_nccl_comm_destroy.argtypes = [c_void_p]
+    L.srj_slab_exchange.argtypes = [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_int64,
+                                    c_int64, c_int64, c_int32, c_void_p]
+    L.srj_slab_exchange_plan.argtypes = [c_int64, c_int32, c_int32, c_int64, c_int64, c_int64,
+                                         c_int32, POINTER(c_int64)]
+    L.srj_allgather_sums.argtypes = [c_void_p, c_int32, c_void_p, c_void_p, c_int64, c_void_p]
+    L.srj_slab_cycle_forward.argtypes = [c_void_p, c_void_p, c_int32, c_int32, c_void_p,
+                                         c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
+                                         c_int32, c_int64, c_int64, c_int64, c_void_p, c_void_p,
+                                         POINTER(c_int32), c_void_p]
     for name in EXPORTED_SYMBOLS:
-        if name not in ("srj_abi_version", "srj_last_error"):
+        if name not in ("srj_abi_version", "srj_last_error", "srj_nccl_last_error"):
             getattr(L, name).restype = c_int32
     L.srj_op_planes.restype = c_int64
 
@@ -174,4 +190,10 @@ def lib():
 def check(rc: int, what: str) -> None:
     if rc != SRJ_OK:
         msg = lib().srj_last_error().decode(errors="replace")
+        raise SrjLibraryError(f"{what} failed (status {rc}): {msg}")
+
+
+def check_nccl(rc: int, what: str) -> None:
+    if rc != SRJ_OK:
+        msg = lib().srj_nccl_last_error().decode(errors="replace")
         raise SrjLibraryError(f"{what} failed (status {rc}): {msg}")

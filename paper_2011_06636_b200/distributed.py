@@ -32,12 +32,14 @@ plug in a numpy engine).
 
 from __future__ import annotations
 
+import ctypes
 import math
 import time
 from dataclasses import dataclass
 
 import numpy as np
 
+from . import _lib
 from .operators import Field, StencilOperator, fill_uniform_rhs
 from .problems import ABSOLUTE_L2, RELATIVE_L2
 from .schemes import MAX_LEVEL, ORDER_GRID_SIZE
@@ -524,19 +526,103 @@ class TbSlab:
         self.x, self.x_alt = self.x_alt, self.x
 
 
+def exchange_plan(s, rank: int, world: int) -> tuple:
+    """srj_slab_exchange_plan of a slab: element offsets (from the first
+    interior point) of the planes sent to / received from rank-1 and rank+1 and
+    the values per message -- the same plan srj_slab_exchange sends by."""
+    plan = (ctypes.c_int64 * 5)()
+    lo, hi = s.owned
+    _lib.check_nccl(_lib.lib().srj_slab_exchange_plan(
+        s.nx, rank, world, lo, hi - lo, s.g_hi, s.ghost, plan), "srj_slab_exchange_plan")
+    return tuple(plan)
+
+
 class LocalTbExchanger(LocalExchanger):
-    """Virtual ranks in one process: deep ghost rows by device copies."""
+    """Virtual ranks in one process: deep ghost rows by device copies, at the
+    offsets of the native exchange plan (srj_slab_exchange_plan)."""
 
     graph_capturable = True
 
     def start_rows(self, slabs, fields):
-        g = slabs[0].ghost
-        for lo, hi, flo, fhi in zip(slabs[:-1], slabs[1:], fields[:-1], fields[1:]):
-            a, b = lo.owned
-            c, d = hi.owned
-            hi.rows(fhi, 0, g).copy_(lo.rows(flo, b - g, b))        # lo's last owned rows
-            lo.rows(flo, b, b + g).copy_(hi.rows(fhi, c, c + g))    # hi's first owned rows
+        world = len(slabs)
+        plans = [exchange_plan(s, r, world) for r, s in enumerate(slabs)]
+        for flo, fhi, plo, phi in zip(fields[:-1], fields[1:], plans[:-1], plans[1:]):
+            m = plo[4]
+            h = flo.halo
+            xl, xh = flo.buf, fhi.buf
+            xh[h + phi[1]:h + phi[1] + m].copy_(xl[h + plo[2]:h + plo[2] + m])  # lo's last owned
+            xl[h + plo[3]:h + plo[3] + m].copy_(xh[h + phi[0]:h + phi[0] + m])  # hi's first owned
         return None
+
+
+class NcclTbExchanger:
+    """One slab per process; the deep-halo exchange and the per-cycle
+    all-gather run natively through libsrj's NCCL entry points
+    (srj_slab_exchange, srj_allgather_sums) on a communicator libsrj creates
+    (srj_nccl_comm_init; the unique id travels over torch.distributed).  With
+    it, TbSlabSolver issues each cycle's forward work as ONE C call
+    (srj_slab_cycle_forward) when the exchange is not split for overlap."""
+
+    graph_capturable = False  # NCCL inside graph capture: not exercised here
+
+    def __init__(self, device, group=None):
+        import torch
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        L = _lib.lib()
+        if not L.srj_nccl_available():
+            raise _lib.SrjLibraryError("libnccl.so.2 not available: "
+                                       + L.srj_nccl_last_error().decode(errors="replace"))
+        uid = (ctypes.c_uint8 * 128)()
+        if self.rank == 0:
+            _lib.check_nccl(L.srj_nccl_unique_id(uid), "srj_nccl_unique_id")
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = (ctypes.c_uint8 * 128).from_buffer_copy(obj[0])
+        self.device = torch.device(device)
+        comm = ctypes.c_void_p()
+        _lib.check_nccl(L.srj_nccl_comm_init(self.world, uid, self.rank, self.device.index or 0,
+                                             ctypes.byref(comm)), "srj_nccl_comm_init")
+        self.comm = comm
+
+    def close(self) -> None:
+        if self.comm:
+            _lib.lib().srj_nccl_comm_destroy(self.comm)
+            self.comm = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _stream(self):
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def start_rows(self, slabs, fields):
+        (s,), (f,) = slabs, fields
+        lo, hi = s.owned
+        _lib.check_nccl(_lib.lib().srj_slab_exchange(
+            s.A.handle, self.comm, self.rank, self.world, f.ptr, lo, hi - lo, s.g_hi, s.ghost,
+            self._stream()), "srj_slab_exchange")
+        return None
+
+    def finish(self, handle) -> None:
+        return None
+
+    def allgather(self, tensors):
+        import torch
+        (t,) = tensors
+        K = t.numel()
+        out = torch.empty(self.world * K, dtype=torch.float64, device=t.device)
+        _lib.check_nccl(_lib.lib().srj_allgather_sums(self.comm, self.world, t.data_ptr(),
+                                                      out.data_ptr(), K, self._stream()),
+                        "srj_allgather_sums")
+        return out.view(self.world, K)
 
 
 class TorchTbExchanger(TorchExchanger):
@@ -703,7 +789,12 @@ class TbSlabSolver(SlabSolver):
         return [torch.zeros(K, dtype=torch.float64, device=s.x.buf.device) for s in self.slabs]
 
     def _global(self, sums, K: int) -> np.ndarray:
-        g = self.ex.allgather(sums).cpu().numpy()  # [world, K]
+        if getattr(self, "_gathered", None) is not None and self._gathered.shape[1] == K \
+                and isinstance(self.ex, NcclTbExchanger):
+            g = self._gathered.cpu().numpy()  # gathered inside srj_slab_cycle_forward
+            self._gathered = None
+        else:
+            g = self.ex.allgather(sums).cpu().numpy()  # [world, K]
         acc = np.zeros(K)
         for r in range(g.shape[0]):  # fixed rank order: identical bits on every rank
             acc = acc + g[r, :K]
@@ -741,6 +832,27 @@ class TbSlabSolver(SlabSolver):
             self._passes(om, self._sums_buffer(Meff + 1), executed)
         return executed, status, float(res[executed]), [float(v) for v in res[1:executed + 1]]
 
+    def _forward_native(self, om, Meff: int):
+        """The whole forward part of the cycle in one libsrj call
+        (srj_slab_cycle_forward: snapshot, passes with NCCL deep-halo
+        exchanges, residual of x_Meff, NCCL all-gather of the sums)."""
+        torch = _torch()
+        (s,) = self.slabs
+        sums = torch.empty(Meff + 1, dtype=torch.float64, device=s.x.buf.device)
+        self._gathered = torch.empty((self.ex.world, Meff + 1), dtype=torch.float64,
+                                     device=s.x.buf.device)
+        lo, hi = s.owned
+        alt = ctypes.c_int32()
+        _lib.check_nccl(_lib.lib().srj_slab_cycle_forward(
+            s.A.handle, self.ex.comm, self.ex.rank, self.ex.world, s.x.ptr, s.x_alt.ptr,
+            s.snap.ptr, s.b.ptr, om.data_ptr(), Meff, self.ghost, lo, hi - lo, s.g_hi,
+            sums.data_ptr(), self._gathered.data_ptr(), ctypes.byref(alt),
+            self.ex._stream()), "srj_slab_cycle_forward")
+        if alt.value:
+            s.swap()
+        self.launches += -(-Meff // self.ghost) + 1
+        return [sums]
+
     def _forward_eager(self, om, Meff: int, sums) -> None:
         for s in self.slabs:
             s.snap.buf.copy_(s.x.buf)
@@ -754,6 +866,8 @@ class TbSlabSolver(SlabSolver):
         per-slab per-sweep sums (device).  Graph mode: the first cycle of a
         key runs eagerly (it also creates every handle and workspace), the
         second captures, later ones replay."""
+        if isinstance(self.ex, NcclTbExchanger) and not self.overlap:
+            return self._forward_native(om, Meff)
         if not self.graphs:
             sums = self._sums_buffer(Meff + 1)
             self._forward_eager(om, Meff, sums)
@@ -802,4 +916,5 @@ def local_tb_slabs(family: str, shape, world: int, ranks, device, face_x=None, f
 __all__ = ["SlabLayout", "Slab", "LocalExchanger", "TorchExchanger", "DeviceEngine",
            "SlabSolver", "local_slabs", "PARTS", "ABSOLUTE_L2", "TB_GHOST", "TB3_GHOST",
            "tb_ghost", "TbSlab",
-           "LocalTbExchanger", "TorchTbExchanger", "TbSlabSolver", "local_tb_slabs"]
+           "LocalTbExchanger", "TorchTbExchanger", "NcclTbExchanger", "TbSlabSolver",
+           "local_tb_slabs", "exchange_plan"]

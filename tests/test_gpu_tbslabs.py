@@ -221,3 +221,42 @@ def test_tb_pass_rejects_more_sweeps_than_the_ring(monkeypatch):
     with pytest.raises(SrjLibraryError):
         A.tb_pass(x, xa, b, om.data_ptr(), 6, 0, 40, sums.data_ptr())
     A.tb_pass(x, xa, b, om.data_ptr(), 4, 0, 40, sums.data_ptr())  # within the ring: fine
+
+
+@pytest.mark.parametrize("name", ["c2_64", "c4_64", "c3_32"])
+def test_nccl_native_slab_cycle_single_rank(name, tmp_path):
+    """The native multi-GPU path (NcclTbExchanger: libsrj's own NCCL
+    communicator; srj_slab_cycle_forward issues snapshot, passes with their
+    deep-halo exchanges, residual and the all-gather as one C call per cycle)
+    on a one-rank job: NCCL loads, the communicator initialises, and the solve
+    reproduces the reference.  (Several ranks need several GPUs; the exchange
+    offsets are the srj_slab_exchange_plan the virtual-rank tests copy by.)"""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2011_06636_b200 as srj
+    from paper_2011_06636_b200 import _lib
+    from paper_2011_06636_b200.distributed import (NcclTbExchanger, TbSlabSolver,
+                                                   local_tb_slabs)
+    assert _lib.lib().srj_nccl_available() == 1, _lib.lib().srj_nccl_last_error()
+    c = P.case(name)
+    fam, n, b, fx, fy = P.case_inputs(c)
+    shape = (n, n, n) if fam == "3d7" else (n, n)
+    dev = torch.device("cuda", 0)
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("gloo", init_method=f"file://{tmp_path}/pg", rank=0,
+                                world_size=1)
+    try:
+        ex = NcclTbExchanger(dev)
+        slabs = local_tb_slabs(fam, shape, 1, [0], dev, face_x=fx, face_y=fy)
+        solver = TbSlabSolver(slabs, ex, overlap=False)
+        solver.load(b=b)
+        rule = srj.StoppingRule(c["norm"], c["tol"], c.get("max_iterations", 10**9))
+        rep = solver.solve(srj.Heuristic(), rule, record_history=False)
+        P.assert_trace_matches(c, _rows(rep), rep.total_iterations, rep.converged,
+                               x=solver.gather())
+        ex.close()
+    finally:
+        if own:
+            dist.destroy_process_group()
