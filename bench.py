@@ -342,7 +342,12 @@ def run_reference(args, rank, world):
         "ms_per_step": sum(c["seconds"] for c in samples) * 1e3 / len(samples),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (SplitMix64 f, seeded)",
-        "config": {"workload": CONFIG_DESC[args.config], "n": npts, "grid": n},
+        "config": {"workload": CONFIG_DESC[args.config], "n": npts, "grid": n,
+                   "step": "a bounded sample of the workload's SRJ sweeps (update + residual + "
+                           "norm, level-14 scheme) on the same grid, not a whole solve: the "
+                           "sweep count of a solve is the GPU arm's (identical scheme "
+                           "sequence, tests/test_gpu_fullsize.py), so compare point-update "
+                           "rates (GLUP/s)"},
         "cpu_baseline": {"value": v, "unit": "GLUP/s", "cores": samples[-1]["cores"],
                          "kind": "port", "sample": samples[-1]["sample"],
                          "host": samples[-1].get("host"),

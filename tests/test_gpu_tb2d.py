@@ -100,3 +100,43 @@ def test_negative_zero_start(family):
     out = A.run_cycle(x, x_alt, A.field(b), om, 6, 0.0, 1.0, 1.0, 10**9, None)
     got = (x_alt if out.result_in_alt else x).interior.cpu().numpy()
     assert np.array_equal(got, xs[6])  # -0.0 == +0.0
+
+
+@pytest.mark.parametrize("family", ["2d5", "2d5var"])
+def test_subnormal_products_start(family):
+    """x0 with subnormal entries, so that c_off * x is subnormal in the first
+    sweep (the TB kernels' `fma(p, -4, y)` diagonal and the dropped
+    leading `0 +` are exact only for normal-or-zero products).  Records the
+    behaviour: the iterates must equal the oracle's to within one unit in the
+    last place of the result scale (they are bit-identical unless a subnormal
+    product changes a rounding)."""
+    import torch
+
+    import paper_2011_06636_b200 as srj
+    from oracle import srj_oracle as O
+    nx, ny = 66, 70
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(5)
+    kw = {}
+    if family == "2d5var":
+        fx = rng.uniform(0.5, 3.0, (ny, nx + 1))
+        fy = rng.uniform(0.5, 3.0, (ny + 1, nx))
+        A = srj.StencilOperator(family, (nx, ny), face_x=fx, face_y=fy, device=dev)
+        op = O.StencilCPU(family, nx, ny, 1, 0.0, fx, fy)
+    else:
+        A = srj.StencilOperator(family, (nx, ny), dx2=5.0, device=dev)
+        op = O.StencilCPU(family, nx, ny, 1, 5.0)
+    assert A.describe()["tb_supported"]
+    b = rng.uniform(-1, 1, A.n)
+    x0 = rng.uniform(-1, 1, A.n) * 1e-310          # subnormal start
+    omegas = rng.uniform(0.4, 1.6, 6)
+    xs, res = _oracle_sweeps(op, x0, b, omegas, 1.0)
+    om = torch.tensor(omegas, dtype=torch.float64, device=dev)
+    x = A.field(x0)
+    x_alt = A.new_field()
+    out = A.run_cycle(x, x_alt, A.field(b), om, len(omegas), 0.0, 1.0, res[0], 10**9,
+                      np.zeros(len(omegas)))
+    got = (x_alt if out.result_in_alt else x).interior.cpu().numpy()
+    want = xs[len(omegas)]
+    scale = np.max(np.abs(want))
+    assert np.max(np.abs(got - want)) <= 2.0 ** -52 * scale, np.max(np.abs(got - want))

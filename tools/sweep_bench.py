@@ -29,7 +29,19 @@ def main():
     for spec in a.cases.split(","):
         fam, n = spec.split(":")
         n = int(n)
-        p = srj.baseline_problem(fam, n, seed=0, device=dev, rhs_on_device=(fam in ("1d3", "2d5", "3d7")))
+        if fam in ("csr2d", "csr3d"):
+            # the generic CSR kernel on a stencil matrix (bytes: x, b, x' + the
+            # CSR row -- 8 B value + 4 B column per entry, 8 B row pointer -- and
+            # 8 B inv_diag)
+            st = srj.StencilOperator("2d5" if fam == "csr2d" else "3d7",
+                                     (n, n) if fam == "csr2d" else (n, n, n))
+            A = srj.SparseMatrix(st.scipy_csr(), device=dev)
+            bpu[fam] = 24 + 12 * A.nnz / A.n + 16
+            p = srj.ProblemInstance(A=A, b=srj.uniform_rhs(0, A.n), x0=np.zeros(A.n),
+                                    stopping_norm="relative_l2")
+        else:
+            p = srj.baseline_problem(fam, n, seed=0, device=dev,
+                                     rhs_on_device=(fam in ("1d3", "2d5", "3d7")))
         A = p.A
         if a.spp > 0:
             A.set_sweeps_per_pass(a.spp)
