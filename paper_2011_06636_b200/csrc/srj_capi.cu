@@ -651,6 +651,7 @@ struct srj_op {
     TbvPlan tbv;                 // var-coef 2D temporal-blocking plan (srj_tbvar.cu)
     Plan3D p3;                   // plane-streaming 3D plan (srj_3d.cuh)
     Plan3V p3v;                  // plane-streaming 3D variable-coefficient plan (srj_3dv.cu)
+    Tb3vPlan tb3v;               // 3D variable-coefficient temporal blocking (srj_tb3v.cu)
     Plan2D p2;                   // tile-streaming 2D plan (srj_2d.cuh)
     // srj_sweep_planes scratch, one set per slot (concurrent launches)
     double* slot_part[kSlots] = {nullptr, nullptr};
@@ -801,6 +802,11 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("3D var-coef plan setup failed: ") + cudaGetErrorString(e));
     }
+    if (op->p3v.supported &&
+        (e = tb3v_plan_init(op->tb3v, g, op->num_sms, op->p3v.fx_pad, op->p3v.fx_pitch)) != cudaSuccess) {
+        srj_op_destroy(op);
+        return fail(SRJ_CUDA_ERROR, std::string("3D var-coef TB setup failed: ") + cudaGetErrorString(e));
+    }
     if ((e = tb_plan_init(op->tb, g, op->num_sms)) != cudaSuccess) {
         srj_op_destroy(op);
         return fail(SRJ_CUDA_ERROR, std::string("temporal-blocking setup failed: ") + cudaGetErrorString(e));
@@ -826,6 +832,10 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
     op->sweeps_per_pass = (op->tb.supported || op->tbv.supported) ? 6
                           : op->tb3.supported                     ? 2
                                                                   : 1;
+    // 3D variable coefficient: the one-sweep plane ring stays the default.  Its
+    // two-sweep kernel (srj_op_set_sweeps_per_pass(op, 2)) halves the DRAM bytes
+    // but both run at the board power cap, the two-sweep one at 1.88 vs 1.33 GHz
+    // and within a few percent (512^3: 131 vs 127 GLUP/s; 256^3: 114 vs 129).
     op->slot_capacity = std::max(op->p3.slots, kApplyBlocksPerSm * op->num_sms);
     for (int s = 0; s < kSlots; ++s) {
         if ((e = cudaMalloc(&op->slot_part[s], op->slot_capacity * sizeof(double))) != cudaSuccess) {
@@ -894,15 +904,22 @@ int srj_op_describe(const srj_op* op, srj_op_info* info) {
     info->cycle_blocks = op->coop_blocks;
     info->cycle_threads = op->coop_threads;
     info->sweeps_per_pass = op->sweeps_per_pass;
-    info->tb_supported = (op->tb.supported || op->tb3.supported || op->tbv.supported) ? 1 : 0;
+    info->tb_supported =
+        (op->tb.supported || op->tb3.supported || op->tbv.supported || op->tb3v.supported) ? 1 : 0;
     const int tbk = tb_variant_for(op->tb, op->sweeps_per_pass);
-    info->tb_blocks = op->tbv.supported ? op->tbv.blocks
-                      : op->tb3.supported ? op->tb3.blocks : op->tb.blocks[tbk];
-    info->tb_occupancy = (op->tbv.supported || op->tb3.supported) ? 1 : op->tb.occupancy;
-    info->tb_tiles = op->tbv.supported ? op->tbv.ntiles
-                     : op->tb3.supported ? op->tb3.ntiles : op->tb.ntiles[tbk];
+    info->tb_blocks = op->tbv.supported    ? op->tbv.blocks
+                      : op->tb3.supported  ? op->tb3.blocks
+                      : op->tb3v.supported ? op->tb3v.blocks
+                                           : op->tb.blocks[tbk];
+    info->tb_occupancy =
+        (op->tbv.supported || op->tb3.supported || op->tb3v.supported) ? 1 : op->tb.occupancy;
+    info->tb_tiles = op->tbv.supported    ? op->tbv.ntiles
+                     : op->tb3.supported  ? op->tb3.ntiles
+                     : op->tb3v.supported ? op->tb3v.ntiles
+                                          : op->tb.ntiles[tbk];
     info->cycle_kernel = (op->sweeps_per_pass > 1 && op->tbv.supported)  ? SRJ_KERNEL_TBVAR
                          : (op->sweeps_per_pass > 1 && op->tb3.supported) ? SRJ_KERNEL_TB3D
+                         : (op->sweeps_per_pass > 1 && op->tb3v.supported) ? SRJ_KERNEL_TB3DV
                          : op->p3.supported                               ? SRJ_KERNEL_PLANE3D
                          : op->p3v.supported                              ? SRJ_KERNEL_PLANE3DV
                          : (op->sweeps_per_pass > 1 && op->tb.supported) ? SRJ_KERNEL_TB2D
@@ -1012,6 +1029,10 @@ int srj_run_cycle(srj_op* op, double* x, double* x_alt, const double* b,
                                   op->partials, op->hist, op->out_i, op->out_d, st, 0, op->g.nz,
                                   nullptr));
         out->launches = 1;
+    } else if (op->sweeps_per_pass > 1 && op->tb3v.supported) {
+        CUDA_TRY(tb3v_launch_cycle(op->tb3v, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,
+                                   op->partials, op->hist, op->out_i, op->out_d, st));
+        out->launches = 1;
     } else if (op->p3v.supported) {
         CUDA_TRY(launch3v_cycle(op->p3v, op->g, x, x_alt, b, omegas_dev, Meff, tol, baseline,
                                 op->partials, op->hist, op->out_i, op->out_d, st));
@@ -1058,6 +1079,7 @@ static int solve_kernel(const srj_op* op) {
     if (op->sweeps_per_pass <= 1) return 0;
     if (op->tbv.supported) return SRJ_KERNEL_TBVAR;
     if (op->tb3.supported) return SRJ_KERNEL_TB3D;
+    if (op->tb3v.supported) return SRJ_KERNEL_TB3DV;
     if (op->tb.supported) return SRJ_KERNEL_TB2D;
     return 0;
 }
@@ -1143,6 +1165,9 @@ int srj_solve(srj_op* op, double* x, double* x_alt, const double* b, const srj_s
     else if (kern == SRJ_KERNEL_TB3D)
         CUDA_TRY(tb3_launch_cycle(op->tb3, g, x, x_alt, b, nullptr, 0, tol, baseline, op->partials,
                                   op->solve_hist, op->out_i, op->out_d, st, 0, g.nz, nullptr, &c));
+    else if (kern == SRJ_KERNEL_TB3DV)
+        CUDA_TRY(tb3v_launch_cycle(op->tb3v, g, x, x_alt, b, nullptr, 0, tol, baseline,
+                                   op->partials, op->solve_hist, op->out_i, op->out_d, st, &c));
     else
         CUDA_TRY(tb_launch_cycle(op->tb, g, x, x_alt, b, nullptr, 0, op->sweeps_per_pass, tol,
                                  baseline, op->partials, op->solve_hist, op->out_i, op->out_d, st,

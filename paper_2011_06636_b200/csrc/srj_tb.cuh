@@ -70,6 +70,22 @@ cudaError_t tb3_launch_cycle(const Tb3Plan& plan, const Geom& g, double* x, doub
                              double* out_d, cudaStream_t st, int z_lo, int z_hi, double* sums,
                              const SolveCtl* ctl = nullptr);
 
+// 3D variable-coefficient temporal blocking (srj_tb3v.cu): 2 sweeps per pass.
+// Shares the 16-byte-pitch face_x copy of the one-sweep plan (Plan3V).
+struct Tb3vPlan {
+    bool supported = false;
+    int blocks = 0, tiles_x = 0, ntiles = 0, zc = 0, items = 0;
+    const double* fx_pad = nullptr;
+    int fx_pitch = 0;
+};
+
+cudaError_t tb3v_plan_init(Tb3vPlan& plan, const Geom& g, int num_sms, const double* fx_pad,
+                           int fx_pitch);
+cudaError_t tb3v_launch_cycle(const Tb3vPlan& plan, const Geom& g, double* x, double* x_alt,
+                              const double* b, const double* omegas, int M, double tol,
+                              double baseline, double* partials, double* hist, int* out_i,
+                              double* out_d, cudaStream_t st, const SolveCtl* ctl = nullptr);
+
 // 2D variable-coefficient temporal blocking (srj_tbvar.cu), up to 6 sweeps per pass.
 struct TbvPlan {
     bool supported = false;

@@ -101,7 +101,8 @@ def test_random_shape_cycle_bitwise(family, seed):
     if stop is not None and any(r <= tol * (1.0 + 1e-9) for r in res[:stop]):
         stop, tol = None, 0.0
     k = M if stop is None else stop
-    spps = {"2d5": [1, 4, 6], "2d5var": [1, 4, 6], "3d7": [1, 2]}.get(family, [None])
+    spps = {"2d5": [1, 4, 6], "2d5var": [1, 4, 6], "3d7": [1, 2], "3d7var": [1, 2]}.get(family,
+                                                                                    [None])
     for spp in spps:
         A = make()
         if spp is not None:
