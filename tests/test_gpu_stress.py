@@ -49,6 +49,7 @@ SELECTION = [
     "tests/test_gpu_random_shapes.py::test_random_shape_cycle_bitwise[1d3var-1]",
     "tests/test_gpu_random_shapes.py::test_random_shape_cycle_bitwise[1d3var-4]",
     "tests/test_gpu_tbslabs.py::test_tb_slabs_graph_replay_matches_reference",
+    "tests/test_gpu_var3d.py",
 ]
 
 
