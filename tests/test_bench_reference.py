@@ -32,6 +32,14 @@ def test_reference_arm_line():
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"] == {"value": d["value"], "unit": "GLUP/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
+    host = d["cpu_baseline"]["host"]
+    assert host["nproc"] >= 1 and "numpy" in host and "OMP_NUM_THREADS" in host
+    stock = d["cpu_baseline"]["reference_stock"]
+    if os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "srj")):
+        assert stock["kind"] == "reference" and stock["value"] > 0   # the unmodified reference
+    else:
+        assert "unavailable" in stock
+    assert "not a whole solve" in d["config"]["step"]
 
 
 def test_reference_arm_rank0_only():
