@@ -830,12 +830,8 @@ int srj_op_create(const srj_op_desc* d, srj_op** out) {
     // coefficients), 2 for the 3D temporally blocked kernel (512^3 sweep: 296 us
     // vs 603 for the HBM-bound plane ring), else one per pass.
     op->sweeps_per_pass = (op->tb.supported || op->tbv.supported) ? 6
-                          : op->tb3.supported                     ? 2
+                          : (op->tb3.supported || op->tb3v.supported) ? 2
                                                                   : 1;
-    // 3D variable coefficient: the one-sweep plane ring stays the default.  Its
-    // two-sweep kernel (srj_op_set_sweeps_per_pass(op, 2)) halves the DRAM bytes
-    // but both run at the board power cap, the two-sweep one at 1.88 vs 1.33 GHz
-    // and within a few percent (512^3: 131 vs 127 GLUP/s; 256^3: 114 vs 129).
     op->slot_capacity = std::max(op->p3.slots, kApplyBlocksPerSm * op->num_sms);
     for (int s = 0; s < kSlots; ++s) {
         if ((e = cudaMalloc(&op->slot_part[s], op->slot_capacity * sizeof(double))) != cudaSuccess) {

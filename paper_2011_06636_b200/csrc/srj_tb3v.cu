@@ -7,33 +7,36 @@
 // diagonal = the six-face sum in the order west, east, south, north, bottom,
 // top, 1/diag a correctly rounded reciprocal), so iterates are bit-identical.
 //
-// Work item = a 60 x 16 owned tile over a run of planes [z0, z1).  Level 1
-// (sweep 1) is computed on the 64 x 18 region around the tile (a one-point
-// ring, two columns on each side to keep the boxes 16-byte aligned) and kept
-// in a three-plane shared-memory ring; level 2 (sweep 2) reads its seven
-// neighbours from that ring and writes the owned points.  Step z (plane z of
-// x arrived): level 1 finishes plane z-1, level 2 finishes plane z-2.  Two
-// copy-engine rings feed it two planes ahead:
-//   ring A (4 stages, plane p): x plane p (68 x 20 box with a two-point ring;
-//          the x map spans the ghost planes) and face_z plane p (64 x 18);
-//   ring B (3 stages, plane p): b, face_x (66 x 18 over the 16-byte-pitch
-//          copy) and face_y (64 x 19).
-// 1/diag of the region (a correctly rounded reciprocal per point) is
-// computed by level 1 and read back by level 2 of the same plane one step
-// later (two-plane ring), so level 2 runs without the reciprocal.
-// Level-1 values outside the grid and on ghost planes are forced to zero (they
-// are level 2's Dirichlet ghosts).  Two block barriers per step (level 1 ->
-// level 2, and before the next step overwrites the level-1 ring slot level 2
-// read).  One CTA of 512 threads per SM (222 KB of shared memory).
+// Work item = a 60 x 14 owned tile over a run of planes [z0, z1); level 1
+// (sweep 1) runs on the 64 x 16 region around it (a one-point ring, two
+// columns each side to keep the boxes 16-byte aligned), level 2 (sweep 2) on
+// the owned points.  Thread (lane, warp) owns region columns 2*lane, 2*lane+1
+// of row `warp` for the whole item and streams in z with its values in
+// registers: x of planes p-1 and p (level 1 at step z = p+1 loads only the new
+// plane p+1 and the in-plane neighbours), its faces, diagonal, 1/diagonal and
+// b of plane p, and its level-1 results of planes p-1, p.  Level 2 is split
+// like the constant-coefficient wavefront (srj_tb3d.cu): right after level 1
+// of plane p has been published (one shared-memory plane, the only values
+// another thread needs), every thread adds up the first six terms of its
+// level-2 sum for plane p in the reference's column order; one step later the
+// seventh (top) term, its own level-1 value of plane p+1, completes it.  One
+// block barrier per plane step.  Copy-engine rings two planes ahead:
+//   ring A (4 stages, plane p): x plane p (68 x 18 box with a two-point ring;
+//          the x map spans the ghost planes) and face_z plane p (64 x 16);
+//   ring B (3 stages, plane p): b, face_x (66 x 16 over the 16-byte-pitch
+//          copy) and face_y (64 x 17).
+// Level-1 values outside the grid and on ghost planes are zero (level 2's
+// Dirichlet ghosts).  512 threads, one CTA per SM.
+//
+// Measured on B200 (level-14 cycle): 512^3 774 us per sweep (173 GLUP/s) vs
+// 1,016 for the one-sweep ring; 256^3 112 vs 130 us.  Progression: level 1 and
+// level 2 both from shared memory with two barriers per step (v2) 983 us --
+// bound by shared-memory bandwidth (~500 B per point pair per step); this
+// register-streaming form reads ~250 B and takes one barrier.  A 384-thread
+// variant without the 128-register cap's small spills measured 851 us.
 //
 // Residuals, stopping and rollback: the shared driver (srj_tbdriver.cuh); the
 // residual of a cycle's final iterate is a level-1-only pass (h = 0).
-//
-// Measured on B200 (512^3, level 14): 983 us per sweep vs 1,021 for the
-// one-sweep ring; solves 131 vs 127 GLUP/s, both at the board power cap -- the
-// two-sweep kernel runs at 1.88 GHz (half the DRAM energy) against 1.33 GHz,
-// so its fp64 and barrier latency, not DRAM, set its pace.  At 256^3 it is
-// slower (114 vs 129: 288 items on 148 SMs).  Opt-in (sweeps_per_pass 2).
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -49,24 +52,21 @@
 namespace srj {
 namespace tb3v {
 constexpr int S = 2;
-constexpr int OX = 60, OY = 16;                 // owned tile
-constexpr int RX = OX + 4, RY = OY + 2;         // level-1 region 64 x 18 (origin ox-2, oy-1)
-constexpr int THREADS = 512;
-constexpr int TROWS = THREADS / RX;             // region rows one pass of the threads covers (8)
-constexpr int XBX = RX + 4, XBY = RY + 2;       // x box 68 x 20 (origin ox-4, oy-2)
+constexpr int OX = 60, OY = 14;                 // owned tile
+constexpr int RX = OX + 4, RY = OY + 2;         // level-1 region 64 x 16 (origin ox-2, oy-1)
+constexpr int THREADS = 32 * RY;                // one warp per region row, 2 columns per lane
+constexpr int XBX = RX + 4, XBY = RY + 2;       // x box 68 x 18 (origin ox-4, oy-2)
 constexpr int XPL = ((XBX * XBY + 15) / 16) * 16;
-constexpr int ZPL = RX * RY;                        // face_z box
-constexpr int ASTRIDE = XPL + ZPL;                  // ring A stage
-constexpr int BPL = RX * RY;                        // b box
-constexpr int FXW = RX + 2;                         // 66: face_x box width (65 faces)
+constexpr int ZPL = RX * RY;                    // face_z box
+constexpr int ASTRIDE = XPL + ZPL;              // ring A stage
+constexpr int BPL = RX * RY;                    // b box
+constexpr int FXW = RX + 2;                     // face_x box width (65 faces, 16-byte multiple)
 constexpr int FXPL = ((FXW * RY + 15) / 16) * 16;
 constexpr int FYPL = ((RX * (RY + 1) + 15) / 16) * 16;  // face_y box (RY + 1 rows)
-constexpr int BSTRIDE = BPL + FXPL + FYPL;          // ring B stage
-constexpr int L1PL = RX * RY;                       // level-1 plane
-constexpr int AST = 4, BST = 3, L1ST = 3, IVST = 2;
-// + 1/diag of the level-1 region, computed by level 1 and reused by level 2
-// one step later (two planes)
-constexpr int NDBL = AST * ASTRIDE + BST * BSTRIDE + L1ST * L1PL + IVST * L1PL;
+constexpr int BSTRIDE = BPL + FXPL + FYPL;      // ring B stage
+constexpr int L1PL = RX * RY;                   // published level-1 plane
+constexpr int AST = 4, BST = 3, L1ST = 2;
+constexpr int NDBL = AST * ASTRIDE + BST * BSTRIDE + L1ST * L1PL;
 constexpr size_t SMEM = (size_t)NDBL * sizeof(double) + 8 * (AST + BST);
 constexpr uint32_t ABYTES = (XBX * XBY + ZPL) * sizeof(double);
 constexpr uint32_t BBYTES = (BPL + FXW * RY + RX * (RY + 1)) * sizeof(double);
@@ -93,10 +93,6 @@ struct Tb3vRing {
     __device__ static __forceinline__ double* l1(int s) {
         return tb3v_smem + tb3v::AST * tb3v::ASTRIDE + tb3v::BST * tb3v::BSTRIDE + s * tb3v::L1PL;
     }
-    __device__ static __forceinline__ double* iv(int s) {
-        return tb3v_smem + tb3v::AST * tb3v::ASTRIDE + tb3v::BST * tb3v::BSTRIDE +
-               tb3v::L1ST * tb3v::L1PL + s * tb3v::L1PL;
-    }
     __device__ static __forceinline__ uint64_t* abar(int s) {
         return reinterpret_cast<uint64_t*>(tb3v_smem + tb3v::NDBL) + s;
     }
@@ -107,7 +103,7 @@ struct Tb3vRing {
 __device__ __forceinline__ void tb3v_issue_a(const CUtensorMap* mx, const CUtensorMap* mz, int ox,
                                              int oy, int p) {
     using namespace tb3v;
-    const int s = (p + 4) & (AST - 1);
+    const int s = (p + 1) & (AST - 1);
     double* st = Tb3vRing::a(s);
     fence_proxy_async();
     mbar_expect_tx(Tb3vRing::abar(s), ABYTES);
@@ -127,47 +123,13 @@ __device__ __forceinline__ void tb3v_issue_b(const Tb3vMaps& m, int ox, int oy, 
     tma_load_3d(st + BPL + FXPL, &m.fy, ox - 2, oy - 1, p, Tb3vRing::bbar(s));
 }
 
-// Seven-point var-coef update of region point (c, r): centre and neighbours
-// from a plane ring whose rows have pitch `pitch` (ctr / dn / up: the point's
-// address in planes p, p-1, p+1); faces from the B stage of plane p and the
-// face_z planes p (bottom) and p+1 (top).  Returns r, writes x'.
-template <bool CACHED>
-__device__ __forceinline__ double tb3v_point(const double* ctr, const double* dn, const double* up,
-                                             int pitch, const double* sb, int c, int r,
-                                             const double* fzb, const double* fzt, double w,
-                                             double& xnew, double* ivp) {
-    using namespace tb3v;
-    const int pi = r * RX + c;
-    const double* sfx = sb + BPL;
-    const double* sfy = sb + BPL + FXPL;
-    const double cw = sfx[r * FXW + c], ce = sfx[r * FXW + c + 1];
-    const double cs = sfy[pi], cn = sfy[pi + RX];
-    const double cb = fzb[pi], ct = fzt[pi];
-    const double d = DADD(DADD(DADD(DADD(DADD(cw, ce), cs), cn), cb), ct);
-    const double xc = ctr[0];
-    double y = DADD(0.0, DMUL(-cb, dn[0]));
-    y = DADD(y, DMUL(-cs, ctr[-pitch]));
-    y = DADD(y, DMUL(-cw, ctr[-1]));
-    y = DADD(y, DMUL(d, xc));
-    y = DADD(y, DMUL(-ce, ctr[1]));
-    y = DADD(y, DMUL(-cn, ctr[pitch]));
-    y = DADD(y, DMUL(-ct, up[0]));
-    const double rr = DSUB(sb[pi], y);
-    // level 1 computes 1/diag and parks it; level 2 (same plane, next step)
-    // reads it back
-    double inv;
-    if constexpr (CACHED) {
-        inv = ivp[pi];
-    } else {
-        inv = __drcp_rn(d);
-        if (ivp) ivp[pi] = inv;
-    }
-    xnew = relax(xc, inv, rr, w);
-    return rr;
+__device__ __forceinline__ double2 lds2(const double* p) {
+    SRJ_ASSERT_SMEM(p, 16, tb3v_smem);
+    return *reinterpret_cast<const double2*>(p);
 }
 
-// One pass over this CTA's items: H = 2 (two sweeps), 1 (one sweep, xout),
-// 0 (residual of the input only, xout == nullptr).
+// One pass over this CTA's items: H = 2 (two sweeps), 1 (one sweep into
+// xout), 0 (residual of the input only, xout == nullptr).
 template <int H>
 __device__ __forceinline__ void tb3v_pass(const TbArgs& a, const Tb3vItems& it, const Tb3vMaps& m,
                                           const CUtensorMap* mx, double* __restrict__ xout,
@@ -175,23 +137,24 @@ __device__ __forceinline__ void tb3v_pass(const TbArgs& a, const Tb3vItems& it, 
                                           double (&acc)[tb3v::S], uint32_t& aph, uint32_t& bph) {
     using namespace tb3v;
     using R = Tb3vRing;
-    const int tid = threadIdx.x;
-    const int c = tid & 63, rq = tid >> 6;  // column, first row (rows rq, rq+8, rq+16)
+    const int lane = threadIdx.x & 31, r = threadIdx.x >> 5;  // region row
+    const int c0 = 2 * lane;                                  // region columns c0, c0+1
     const int nx = a.g.nx, ny = a.g.ny, nz = a.g.nz;
     const long long plane = (long long)nx * ny;
     const double w0 = H >= 1 ? __ldg(om) : 0.0, w1 = H == 2 ? __ldg(om + 1) : 0.0;
+    // owned columns / rows of the tile (region columns 2 .. 61, rows 1 .. 14)
+    const bool lane_own = lane >= 1 && lane <= 30, row_own = r >= 1 && r <= OY;
     for (int item = blockIdx.x; item < it.items; item += gridDim.x) {
         const int tile = item % it.ntiles, zci = item / it.ntiles;
         const int ox = (tile % it.tiles_x) * OX, oy = (tile / it.tiles_x) * OY;
         const int z0 = zci * it.zc, z1 = min(z0 + it.zc, nz);
-        // level-1 planes [L0, L1)
-        const int L0 = H == 2 ? z0 - 1 : z0, L1 = H == 2 ? z1 + 1 : z1;
-        if (tid == 0) {
+        const int L0 = H == 2 ? z0 - 1 : z0, L1 = H == 2 ? z1 + 1 : z1;  // level-1 planes
+        if (threadIdx.x == 0) {
             for (int p = L0 - 1; p <= min(L0 + 2, L1); ++p) tb3v_issue_a(mx, &m.fz, ox, oy, p);
-            for (int p = L0; p <= min(L0 + 1, L1 - 1); ++p) tb3v_issue_b(m, ox, oy, p);
+            for (int p = L0; p <= min(L0 + 2, L1 - 1); ++p) tb3v_issue_b(m, ox, oy, p);
         }
         auto wait_a = [&](int p) {
-            const int s = (p + 4) & (AST - 1);
+            const int s = (p + 1) & (AST - 1);
             mbar_wait(R::abar(s), (aph >> s) & 1u);
             aph ^= 1u << s;
         };
@@ -200,87 +163,130 @@ __device__ __forceinline__ void tb3v_pass(const TbArgs& a, const Tb3vItems& it, 
             mbar_wait(R::bbar(s), (bph >> s) & 1u);
             bph ^= 1u << s;
         };
+        const int gx = ox - 2 + c0, gy = oy - 1 + r;  // grid point of column c0
+        const bool in0 = gx >= 0 && gx < nx && gy >= 0 && gy < ny;
+        const bool in1 = gx + 1 >= 0 && gx + 1 < nx && gy >= 0 && gy < ny;
+        // owned column pair (even nx: both or neither inside the grid)
+        const bool own = lane_own && row_own && gx < nx && gy < ny;
+        const int xb_i = (r + 1) * XBX + c0 + 2;  // x box index of (c0, r)
+        const int ri = r * RX + c0;               // region index of (c0, r)
+        // streamed registers of the thread's two points
+        double X0[2], X1[2], fzb[2];              // x(p-1), x(p), face_z(p)
+        double Lp[2] = {0.0, 0.0};                // level-1 value of plane p-1
+        double yp2[2], ct2[2], iv2[2], b2[2], lc2[2];  // level-2 partial of plane p-1
         wait_a(L0 - 1);
         wait_a(L0);
-        const int gx = ox - 2 + c;
-        const bool colin = gx >= 0 && gx < nx;
-        const bool colown = c >= 2 && c <= 61 && gx < nx;
+        {
+            const double2 v0 = lds2(R::a(L0 & (AST - 1)) + xb_i);         // x(L0 - 1)
+            const double2 v1 = lds2(R::a((L0 + 1) & (AST - 1)) + xb_i);   // x(L0)
+            const double2 f1 = lds2(R::a((L0 + 1) & (AST - 1)) + XPL + ri);  // face_z(L0)
+            X0[0] = v0.x; X0[1] = v0.y;
+            X1[0] = v1.x; X1[1] = v1.y;
+            fzb[0] = f1.x; fzb[1] = f1.y;
+        }
         for (int z = L0 + 1; z <= L1; ++z) {
-            const int p1 = z - 1;  // level-1 plane
+            const int p = z - 1;  // level-1 plane of this step
             wait_a(z);
-            wait_b(p1);
-            // ---- level 1 over the 64 x 10 region of plane p1
-            {
-                const double* xm = R::a((p1 - 1 + 4) & (AST - 1));  // x planes p1-1, p1, p1+1
-                const double* xc = R::a((p1 + 4) & (AST - 1));
-                const double* xp = R::a((p1 + 1 + 4) & (AST - 1));
-                const double* sb = R::b((p1 + 3) % BST);
-                double* ivp = R::iv((p1 + 2) & 1);
-                const bool plane_own = accumulate && p1 >= z0 && p1 < z1;
-                const bool plane_in = p1 >= 0 && p1 < nz;
-                double* l1 = R::l1((p1 + 3) % 3);
+            wait_b(p);
+            const double* ac = R::a((p + 1) & (AST - 1));  // plane p: x neighbours
+            const double* at = R::a((z + 1) & (AST - 1));  // plane p+1: x, face_z
+            const double* sb = R::b((p + 3) % BST);
+            // ---- level 1 of plane p at the thread's two points
+            const double2 xt = lds2(at + xb_i);
+            const double2 fzt = lds2(at + XPL + ri);
+            const double2 xwp = lds2(ac + xb_i - 2), xep = lds2(ac + xb_i + 2);
+            const double2 xs = lds2(ac + xb_i - XBX), xnn = lds2(ac + xb_i + XBX);
+            const double2 bb = lds2(sb + ri);
+            const double* sfx = sb + BPL + r * FXW + c0;
+            const double2 fx01 = lds2(sfx);
+            const double fx2 = sfx[2];
+            const double2 fys = lds2(sb + BPL + FXPL + ri), fyn = lds2(sb + BPL + FXPL + ri + RX);
+            const double cw[2] = {fx01.x, fx01.y}, ce[2] = {fx01.y, fx2};
+            const double cs[2] = {fys.x, fys.y}, cn[2] = {fyn.x, fyn.y};
+            const double ct[2] = {fzt.x, fzt.y};
+            const double xw[2] = {xwp.y, X1[0]}, xe[2] = {X1[1], xep.x};
+            const double xsv[2] = {xs.x, xs.y}, xnv[2] = {xnn.x, xnn.y}, xtv[2] = {xt.x, xt.y};
+            const double bv[2] = {bb.x, bb.y};
+            const bool plane_in = p >= 0 && p < nz;
+            const bool plane_own = p >= z0 && p < z1;
+            double d[2], iv[2], l1[2];
 #pragma unroll
-                for (int q = 0; q < (RY + TROWS - 1) / TROWS; ++q) {
-                    const int r = rq + TROWS * q;
-                    if (r < RY) {
-                        const int bi = (r + 1) * XBX + c + 2;  // x box index of (c, r)
-                        double xnew;
-                        const double rr = tb3v_point<false>(xc + bi, xm + bi, xp + bi, XBX, sb, c,
-                                                            r, xc + XPL, xp + XPL, w0, xnew,
-                                                            H == 2 ? ivp : nullptr);
-                        const int gy = oy - 1 + r;
-                        const bool in = plane_in && colin && gy >= 0 && gy < ny;
-                        const bool own = colown && r >= 1 && r <= OY && gy < ny;
-                        if (plane_own && own) acc[0] = fma(rr, rr, acc[0]);
-                        if constexpr (H == 2) {
-                            l1[r * RX + c] = in ? xnew : 0.0;
-                        } else if constexpr (H == 1) {
-                            if (own && p1 >= z0 && p1 < z1) {
-                                SRJ_ASSERT(gx < nx && gy < ny && p1 < nz);
-                                xout[(long long)p1 * plane + (long long)gy * nx + gx] = xnew;
-                            }
-                        }
-                    }
-                }
+            for (int j = 0; j < 2; ++j) {
+                d[j] = DADD(DADD(DADD(DADD(DADD(cw[j], ce[j]), cs[j]), cn[j]), fzb[j]), ct[j]);
+                double y = DADD(0.0, DMUL(-fzb[j], X0[j]));
+                y = DADD(y, DMUL(-cs[j], xsv[j]));
+                y = DADD(y, DMUL(-cw[j], xw[j]));
+                y = DADD(y, DMUL(d[j], X1[j]));
+                y = DADD(y, DMUL(-ce[j], xe[j]));
+                y = DADD(y, DMUL(-cn[j], xnv[j]));
+                y = DADD(y, DMUL(-ct[j], xtv[j]));
+                const double rr = DSUB(bv[j], y);
+                iv[j] = __drcp_rn(d[j]);
+                const double xn = relax(X1[j], iv[j], rr, w0);
+                const bool inj = plane_in && (j == 0 ? in0 : in1);
+                l1[j] = inj ? xn : 0.0;
+                if (accumulate && own && plane_own) acc[0] = fma(rr, rr, acc[0]);
             }
-            __syncthreads();
-            // ---- level 2 over the owned 60 x 8 tile of plane p2 = z - 2
             if constexpr (H == 2) {
-                const int p2 = z - 2;
-                if (p2 >= z0) {
-                    const double* lm = R::l1((p2 - 1 + 3) % 3);
-                    const double* lc = R::l1((p2 + 3) % 3);
-                    const double* lp = R::l1((p2 + 1 + 3) % 3);
-                    const double* sb = R::b((p2 + 3) % BST);
-                    const double* ivp = R::iv((p2 + 2) & 1);
-                    const double* fzb = R::a((p2 + 4) & (AST - 1)) + XPL;
-                    const double* fzt = R::a((p2 + 1 + 4) & (AST - 1)) + XPL;
+                *reinterpret_cast<double2*>(R::l1((p + 2) & 1) + ri) = make_double2(l1[0], l1[1]);
+                // finish level 2 of plane p-1: the top term is this level-1 value
+                if (own && p - 1 >= z0 && p - 1 < z1) {
+                    double xo[2];
 #pragma unroll
-                    for (int q = 0; q < OY / TROWS; ++q) {
-                        const int r = 1 + rq + TROWS * q;  // region rows 1 .. OY
-                        const int li = r * RX + c;
-                        if (colown) {
-                            double xnew;
-                            const double rr = tb3v_point<true>(lc + li, lm + li, lp + li, RX, sb,
-                                                               c, r, fzb, fzt, w1, xnew,
-                                                               const_cast<double*>(ivp));
-                            const int gy = oy - 1 + r;
-                            if (gy < ny) {
-                                if (accumulate) acc[1] = fma(rr, rr, acc[1]);
-                                SRJ_ASSERT(gx < nx && p2 < nz);
-                                xout[(long long)p2 * plane + (long long)gy * nx + gx] = xnew;
-                            }
-                        }
+                    for (int j = 0; j < 2; ++j) {
+                        const double y = DADD(yp2[j], DMUL(-ct2[j], l1[j]));
+                        const double rr = DSUB(b2[j], y);
+                        xo[j] = relax(lc2[j], iv2[j], rr, w1);
+                        if (accumulate) acc[1] = fma(rr, rr, acc[1]);
+                    }
+                    SRJ_ASSERT(gx + 1 < nx && gy < ny && p - 1 < nz);
+                    *reinterpret_cast<double2*>(xout + (long long)(p - 1) * plane + (long long)gy * nx + gx) =
+                        make_double2(xo[0], xo[1]);
+                }
+            } else if constexpr (H == 1) {
+                if (own && plane_own) {
+                    SRJ_ASSERT(gx + 1 < nx && gy < ny && p < nz);
+                    *reinterpret_cast<double2*>(xout + (long long)p * plane + (long long)gy * nx + gx) =
+                        make_double2(l1[0], l1[1]);
+                }
+            }
+            __syncthreads();  // level-1 plane p published; stages of plane p-1 (A) / p (B) free
+            if constexpr (H == 2) {
+                // first six level-2 terms of plane p (bottom, south, west, diag, east, north)
+                if (own && plane_own) {
+                    const double* lp = R::l1((p + 2) & 1);
+                    const double2 ls = lds2(lp + ri - RX), ln = lds2(lp + ri + RX);
+                    const double2 lw = lds2(lp + ri - 2), le = lds2(lp + ri + 2);
+                    const double lsv[2] = {ls.x, ls.y}, lnv[2] = {ln.x, ln.y};
+                    const double lwv[2] = {lw.y, l1[0]}, lev[2] = {l1[1], le.x};
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        double y = DADD(0.0, DMUL(-fzb[j], Lp[j]));
+                        y = DADD(y, DMUL(-cs[j], lsv[j]));
+                        y = DADD(y, DMUL(-cw[j], lwv[j]));
+                        y = DADD(y, DMUL(d[j], l1[j]));
+                        y = DADD(y, DMUL(-ce[j], lev[j]));
+                        yp2[j] = DADD(y, DMUL(-cn[j], lnv[j]));
+                        ct2[j] = ct[j];
+                        iv2[j] = iv[j];
+                        b2[j] = bv[j];
+                        lc2[j] = l1[j];
                     }
                 }
-                __syncthreads();  // level-1 slot of plane p2-1 is rewritten next step
             }
-            if (tid == 0) {
-                // plane z-2's stages are free (ring A: x and face_z; ring B)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                Lp[j] = l1[j];
+                X0[j] = X1[j];
+                X1[j] = xtv[j];
+                fzb[j] = ct[j];
+            }
+            if (threadIdx.x == 0) {
                 if (z + 2 <= L1) tb3v_issue_a(mx, &m.fz, ox, oy, z + 2);
-                if (z + 1 <= L1 - 1) tb3v_issue_b(m, ox, oy, z + 1);
+                if (z + 2 <= L1 - 1) tb3v_issue_b(m, ox, oy, z + 2);
             }
         }
+        __syncthreads();  // the next item's prologue reuses the rings
     }
 }
 

@@ -20,9 +20,8 @@ pytestmark = pytest.mark.gpu
 
 CASES = ["c1_seed0", "poisson1d_100_heuristic", "poisson1d_100_increasing", "fixed5_tol_tiny",
          "increasing_clamp", "tiny_1d_n1", "c2_32", "c2_64", "c3_16", "c4_32",
-         "budget_midcycle_2d", "fixed2362_3d", "poisson3d_24_ones", "c1v_1024", "c1v_100_s2"]
-# (3D variable coefficient: the device loop runs with sweeps_per_pass = 2,
-# tests/test_gpu_var3d.py)
+         "budget_midcycle_2d", "fixed2362_3d", "poisson3d_24_ones", "c1v_1024", "c1v_100_s2",
+         "c3v_12", "c3v_24_budget"]
 
 
 def _solve(c, device_loop, record_history=True, spp=None):
