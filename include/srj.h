@@ -157,8 +157,10 @@ enum srj_cycle_kernel {
     SRJ_KERNEL_SMALL1D = 7,    /* single-CTA shared-memory 1D cycle (n <= 8192) */
     SRJ_KERNEL_REG1D = 8,      /* single-CTA register-resident 1D cycle (n <= 4096) */
     SRJ_KERNEL_PLANE3DV = 9,   /* TMA plane streaming 3D variable coefficient   */
-    SRJ_KERNEL_TB3DV = 10      /* temporally blocked 3D variable coefficient
+    SRJ_KERNEL_TB3DV = 10,     /* temporally blocked 3D variable coefficient
                                   (2 sweeps per pass when sweeps_per_pass > 1)  */
+    SRJ_KERNEL_TBS2D = 11      /* temporally blocked 2D, skewed tiles (whole-grid
+                                  cycles and solves at 5-6 sweeps per pass)     */
 };
 
 /* Temporally blocked 2D kernel used when sweeps_per_pass > 1. */

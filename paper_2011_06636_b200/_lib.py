@@ -97,7 +97,8 @@ class OpInfo(ctypes.Structure):
                7: "srj::k_small_cycle_1d (single-CTA shared-memory cycle)",
                8: "srj::k_reg_cycle_1d (single-CTA register-resident cycle)",
                9: "srj::k_cycle3dv (TMA plane ring, variable coefficient)",
-               10: "srj::k_tb3v_cycle (TMA z-wavefront temporal blocking, variable coefficient)"}
+               10: "srj::k_tb3v_cycle (TMA z-wavefront temporal blocking, variable coefficient)",
+               11: "srj::k_tbs_cycle (TMA temporal blocking, skewed tiles)"}
 
     def as_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}

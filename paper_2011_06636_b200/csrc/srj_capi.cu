@@ -864,6 +864,7 @@ int srj_op_destroy(srj_op* op) {
     cudaFree(op->solve_hist);
     plan2d_free(op->p2);
     tbv_plan_free(op->tbv);
+    tbs_plan_free(op->tb);
     plan3v_free(op->p3v);
     delete op;
     return SRJ_OK;
@@ -903,21 +904,25 @@ int srj_op_describe(const srj_op* op, srj_op_info* info) {
     info->tb_supported =
         (op->tb.supported || op->tb3.supported || op->tbv.supported || op->tb3v.supported) ? 1 : 0;
     const int tbk = tb_variant_for(op->tb, op->sweeps_per_pass);
+    const bool skew = op->tb.supported && tb_uses_skew(op->tb, op->sweeps_per_pass);
     info->tb_blocks = op->tbv.supported    ? op->tbv.blocks
                       : op->tb3.supported  ? op->tb3.blocks
                       : op->tb3v.supported ? op->tb3v.blocks
+                      : skew               ? op->tb.skew_blocks
                                            : op->tb.blocks[tbk];
     info->tb_occupancy =
         (op->tbv.supported || op->tb3.supported || op->tb3v.supported) ? 1 : op->tb.occupancy;
     info->tb_tiles = op->tbv.supported    ? op->tbv.ntiles
                      : op->tb3.supported  ? op->tb3.ntiles
                      : op->tb3v.supported ? op->tb3v.ntiles
+                     : skew               ? op->tb.skew_blocks * op->tb.skew_tpc
                                           : op->tb.ntiles[tbk];
     info->cycle_kernel = (op->sweeps_per_pass > 1 && op->tbv.supported)  ? SRJ_KERNEL_TBVAR
                          : (op->sweeps_per_pass > 1 && op->tb3.supported) ? SRJ_KERNEL_TB3D
                          : (op->sweeps_per_pass > 1 && op->tb3v.supported) ? SRJ_KERNEL_TB3DV
                          : op->p3.supported                               ? SRJ_KERNEL_PLANE3D
                          : op->p3v.supported                              ? SRJ_KERNEL_PLANE3DV
+                         : (op->sweeps_per_pass > 1 && skew)              ? SRJ_KERNEL_TBS2D
                          : (op->sweeps_per_pass > 1 && op->tb.supported) ? SRJ_KERNEL_TB2D
                          : op->p2.supported                               ? SRJ_KERNEL_TILE2D
                          : reg1d_ok(op->g) ? SRJ_KERNEL_REG1D

@@ -556,7 +556,20 @@ cudaError_t tb_plan_init(TbPlan& plan, const Geom& g, int num_sms) {
     plan_tiles<0>(plan, g, num_sms);
     plan_tiles<1>(plan, g, num_sms);
     plan.supported = true;
-    return cudaSuccess;
+    // region rows per CTA and pass with the square S = 6 tiles (rounds x RY)
+    plan.tile_rows = ((plan.ntiles[1] + plan.blocks[1] - 1) / plan.blocks[1]) * tb2d::Cfg<1>::RY;
+    return tbs_plan_init(plan, g, num_sms);
+}
+
+// The skewed-tile kernel serves whole-grid cycles and solves at 5-6 sweeps per
+// pass when it computes fewer region rows per CTA and pass than the square
+// tiles (small grids: one 96-row tile per CTA loses to one 72-row tile).
+// SRJ_TB_SKEW=0 / 1 forces the choice (tuning and tests).
+bool tb_uses_skew(const TbPlan& plan, int s) {
+    if (!plan.skew || s <= tb2d::Cfg<0>::S || plan.reserved > 0) return false;
+    if (const char* v = getenv("SRJ_TB_SKEW"))
+        if (atoi(v) == 1) return true;
+    return plan.skew_rows < plan.tile_rows;
 }
 
 template <int K>
@@ -604,6 +617,8 @@ cudaError_t tb_launch_cycle(const TbPlan& plan, const Geom& g, double* x, double
     a.hist = hist;
     a.out_i = out_i;
     a.out_d = out_d;
+    if (sums == nullptr && row_lo == 0 && row_hi == g.ny && tb_uses_skew(plan, s))
+        return tbs_launch_cycle(plan, g, a, x, x_alt, b, st);
     switch (k) {
         case 1: return launch_variant<1>(plan, g, a, x, x_alt, b, st);
         default: return launch_variant<0>(plan, g, a, x, x_alt, b, st);

@@ -19,7 +19,22 @@ struct TbPlan {
     int small_variant = -1;         // forced variant (SRJ_TB_VARIANT), -1: by sweeps per pass
     int occupancy = 0;              // min resident CTAs per SM over the variants
     int reserved = 0;               // SMs left free (srj_op_set_reserved_sms)
+    // skewed-tile kernel (srj_tbs.cu): whole-grid cycles / solves at 5-6 sweeps per pass
+    bool skew = false;
+    int skew_tpc = 0;               // tile budget per CTA
+    int skew_blocks = 0;            // CTAs that own tiles
+    int skew_rows = 0, tile_rows = 0;  // region rows per CTA and pass: skewed / square tiles
+    void* skew_tab = nullptr;       // device int4[blocks * tpc]: {ox, oy, lo, hi}
 };
+
+struct TbArgs;
+// Skewed-tile kernel (srj_tbs.cu): plan (tile table on the device), launch.
+cudaError_t tbs_plan_init(TbPlan& plan, const Geom& g, int num_sms);
+void tbs_plan_free(TbPlan& plan);
+cudaError_t tbs_launch_cycle(const TbPlan& plan, const Geom& g, TbArgs& a, double* x, double* x_alt,
+                             const double* b, cudaStream_t st);
+// True when a whole-grid launch at s sweeps per pass runs the skewed-tile kernel.
+bool tb_uses_skew(const TbPlan& plan, int s);
 
 // Decide whether the operator has a temporal-blocking kernel and size its grid.
 cudaError_t tb_plan_init(TbPlan& plan, const Geom& g, int num_sms);

@@ -49,6 +49,10 @@ struct TbArgs {
     double* sums;
     // Device-resident solve (the kernels' SOLVE instantiation only).
     SolveCtl ctl;
+    // Skewed-tile kernel (srj_tbs.cu): CTA c runs tab[c*tpc .. c*tpc + tpc),
+    // {ox, oy, lo, hi} per tile, until an entry with hi <= lo.
+    const int4* tab = nullptr;
+    int tpc = 0;
 };
 
 struct TbCycleResult {
