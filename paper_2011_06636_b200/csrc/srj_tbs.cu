@@ -37,6 +37,9 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#ifdef SRJ_TBS_TIMING
+#include <cstdio>
+#endif
 #include <cstdlib>
 #include <vector>
 
@@ -48,6 +51,9 @@
 
 #ifndef SRJ_TBS_ILP8
 #define SRJ_TBS_ILP8 true
+#endif
+#ifndef SRJ_TBS_NW
+#define SRJ_TBS_NW 16
 #endif
 
 namespace srj {
@@ -74,7 +80,9 @@ struct CfgT {
     static constexpr int OFF_X = 0, OFF_B = XSTAGE, OFF_H = OFF_B + 2 * BSTAGE,
                          OFF_C = OFF_H + 2 * HBUF, OFF_BAR = OFF_C + 2 * CARRY;
     static constexpr int MAXT = 128;              // tile descriptors kept in shared memory
-    static constexpr int OFF_DESC = OFF_BAR + 8;  // int4[MAXT]
+    // mbarriers: TMA full, 2 hand-off rounds, stage consumed
+    static constexpr int OFF_OM = OFF_BAR + 4;             // the pass's omegas [S] (+ pad)
+    static constexpr int OFF_DESC = OFF_OM + 8;            // int4[MAXT]
     static constexpr size_t SMEM = (size_t)(OFF_DESC + 2 * MAXT) * sizeof(double);
     static constexpr bool ILP8 = ILP8_;
     static constexpr uint32_t TX_BYTES = (uint32_t)((XSTAGE + BSTAGE) * sizeof(double));
@@ -82,7 +90,7 @@ struct CfgT {
     static_assert((XSTAGE * 8) % 128 == 0 && (BSTAGE * 8) % 128 == 0, "TMA destinations");
 };
 
-using Cfg = CfgT<16, 6, SRJ_TBS_ILP8>;  // 64 x 96 tiles, 512 threads, 128 registers
+using Cfg = CfgT<SRJ_TBS_NW, 6, SRJ_TBS_ILP8>;  // 64 x 96 tiles, 512 threads, 128 registers
 
 }  // namespace tbs
 
@@ -100,9 +108,11 @@ struct TbsLayout {
     __device__ static __forceinline__ uint64_t* hbar(int i) {
         return reinterpret_cast<uint64_t*>(tbs_smem + C::OFF_BAR) + 1 + i;
     }
+    // stage consumed (one arrival per warp): the next tile's copy may start
     __device__ static __forceinline__ uint64_t* sempty() {
         return reinterpret_cast<uint64_t*>(tbs_smem + C::OFF_BAR) + 3;
     }
+    __device__ static __forceinline__ double* om() { return tbs_smem + C::OFF_OM; }
     __device__ static __forceinline__ int4* desc_ptr() {
         return reinterpret_cast<int4*>(tbs_smem + C::OFF_DESC);
     }
@@ -154,9 +164,38 @@ struct TbsState {
     uint32_t tc;     // tiles started (b stage, carry and stage-consumed parity)
 };
 
+#ifdef SRJ_TBS_TIMING  // (tuning only) clock ticks of CTA 0, first / last warp, third tile
+__shared__ long long tbs_tm[2][40];
+#define TBS_TICK(k)                                                                        \
+    do {                                                                                   \
+        if (blockIdx.x == 0 && st.tc == 2u && (threadIdx.x & 31) == 0 &&                   \
+            (threadIdx.x == 0 || threadIdx.x == 32 * (tbs::Cfg::NW - 1)))                  \
+            tbs_tm[threadIdx.x != 0][k] = clock64();                                       \
+    } while (0)
+#else
+#define TBS_TICK(k) ((void)0)
+#endif
+
+// Hand-off of the published rows: one mbarrier round per level (every warp
+// arrives after publishing, waits before reading).  g = st.hb + level numbers
+// the rounds across tiles, passes and cycles (barrier g & 1, use g >> 1).
+template <class C>
+struct TbsSync {
+    using L = TbsLayout<C>;
+    __device__ static __forceinline__ void wait_read(int level, const TbsState& st) {
+        const uint32_t g = st.hb + level;
+        mbar_wait(L::hbar(g & 1), (g >> 1) & 1);
+    }
+    __device__ static __forceinline__ void done_write(int lane, int level, const TbsState& st) {
+        const uint32_t g = st.hb + level;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(L::hbar(g & 1));
+    }
+};
+
 // NR rows (2*NR chains) of new slots V0 .. V0+NR-1 from this thread's own old
 // slots: south = old slot v-2, centre = old slot v-1, north = old slot v.
-template <class C, int V0, int NR, int T, bool MASKED>
+template <class C, int V0, int NR, bool MASKED>
 __device__ __forceinline__ void tbs_rows(const double (&X)[C::V][2], const double (&P)[C::V][2],
                                          const double (&pw)[C::V], const double (&pe)[C::V],
                                          double (&Xn)[C::V][2], double (&sq)[4], double w,
@@ -184,9 +223,8 @@ __device__ __forceinline__ void tbs_rows(const double (&X)[C::V][2], const doubl
     for (int k = 0; k < NP; ++k) y[k] = DADD(y[k], P[V0 + (k >> 1)][k & 1]);
 #pragma unroll
     for (int k = 0; k < NP; k += 2) {
-        const int v = V0 + (k >> 1);
         double bv[2];
-        tbs_lds2(bv, boff + (v - T) * RX);
+        tbs_lds2(bv, boff + (V0 + (k >> 1)) * RX);
         rr[k] = DSUB(bv[0], y[k]);
         rr[k + 1] = DSUB(bv[1], y[k + 1]);
     }
@@ -222,9 +260,8 @@ __device__ __forceinline__ void tbs_tile_sweeps(double (&X)[C::V][2], double (&P
     const int c0 = lane * 2;
 #pragma unroll
     for (int t = 0; t < H; ++t) {
-        const double w = __ldg(omegas + t);
+        const double w = L::om()[t];
         const unsigned im = inmask >> (5 - t), am = accmask >> (5 - t);
-        const uint32_t round = st.hb + t;
         double pw[V], pe[V];  // p across the lane boundary of the centre rows (old slots 0..V-2)
 #pragma unroll
         for (int v = 1; v < V - 1; ++v) {
@@ -235,13 +272,15 @@ __device__ __forceinline__ void tbs_tile_sweeps(double (&X)[C::V][2], double (&P
         double sq[4] = {0.0, 0.0, 0.0, 0.0};
         // new slots 2..5: everything they need is this thread's
         if constexpr (C::ILP8) {
-            tbs_rows<C, 2, 4, 0, MASKED>(X, P, pw, pe, Xn, sq, w, inv, im, am, boff - t * RX);
+            tbs_rows<C, 2, 4, MASKED>(X, P, pw, pe, Xn, sq, w, inv, im, am, boff - t * RX);
         } else {
-            tbs_rows<C, 4, 2, 0, MASKED>(X, P, pw, pe, Xn, sq, w, inv, im, am, boff - t * RX);
-            tbs_rows<C, 2, 2, 0, MASKED>(X, P, pw, pe, Xn, sq, w, inv, im, am, boff - t * RX);
+            tbs_rows<C, 4, 2, MASKED>(X, P, pw, pe, Xn, sq, w, inv, im, am, boff - t * RX);
+            tbs_rows<C, 2, 2, MASKED>(X, P, pw, pe, Xn, sq, w, inv, im, am, boff - t * RX);
         }
         // level-t rows of the warp above (t = 0: published at tile start)
-        mbar_wait(L::hbar(round & 1), (round >> 1) & 1);
+        TBS_TICK(1 + 3 * t);
+        TbsSync<C>::wait_read(t, st);
+        TBS_TICK(2 + 3 * t);
         double p4[2], p5[2], x5[2];
         {
             const int ro = L::rd_off(warp, t, st.hb, st.tc) + c0;
@@ -300,18 +339,19 @@ __device__ __forceinline__ void tbs_tile_sweeps(double (&X)[C::V][2], double (&P
 #pragma unroll
         for (int v = 0; v < V; ++v)
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                X[v][j] = Xn[v][j];
-                P[v][j] = DMUL(coff, Xn[v][j]);
-            }
-        if (t + 1 < H) {
+            for (int j = 0; j < 2; ++j) X[v][j] = Xn[v][j];
+        if (t + 1 < H) {  // (the products of the pass's last level are never used)
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) P[v][j] = DMUL(coff, X[v][j]);
             const int wo = L::wr_off(warp, t + 1, st.hb, st.tc) + c0;
             tbs_sts2(wo, P[V - 2]);
             tbs_sts2(wo + RX, P[V - 1]);
             tbs_sts2(wo + 2 * RX, X[V - 1]);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(L::hbar((round + 1) & 1));
+            TbsSync<C>::done_write(lane, t + 1, st);
         }
+        TBS_TICK(3 + 3 * t);
     }
 }
 
@@ -359,6 +399,10 @@ __device__ __forceinline__ void tbs_pass(const TbArgs& a, const CUtensorMap* tm_
     const int nx = a.g.nx, ny = a.g.ny;
     const double coff = a.g.c_off;
     if (ntile == 0) return;
+    // Pass start (every warp is past the previous pass's block barriers): the
+    // pass's omegas into shared memory.
+    if (threadIdx.x < h) L::om()[threadIdx.x] = __ldg(om + threadIdx.x);
+    __syncthreads();
     if (threadIdx.x == 0 && !first_issued) {
         const int4 d = L::desc(0);
         tbs_issue<C>(tm_in, tm_b, d.x, d.y, st.tc);
@@ -381,6 +425,9 @@ __device__ __forceinline__ void tbs_pass(const TbArgs& a, const CUtensorMap* tm_
             const bool allown = R0 - 6 >= lo && R0 + 4 < hi;
             const bool noneown = (R0 + 4 < lo || R0 - 6 >= hi) && R0 - 6 >= 0 && R0 + 4 < ny;
             masked = !(colsok && (allown || noneown));
+#ifdef SRJ_TBS_FORCEMASK  // (timing experiment: every warp takes the masked path)
+            masked = true;
+#endif
             if (masked) {
                 const bool cin = gx0 >= 0 && gx0 < nx;  // a lane's column pair is inside as a whole (even nx)
                 inmask = cin ? tbs_range_mask(6 - R0, ny + 6 - R0) : 0u;
@@ -390,7 +437,9 @@ __device__ __forceinline__ void tbs_pass(const TbArgs& a, const CUtensorMap* tm_
             }
         }
         const unsigned accmask = accumulate ? ownmask : 0u;
+        TBS_TICK(30);
         mbar_wait(L::bar(), st.phase);
+        TBS_TICK(31);
         st.phase ^= 1u;
         double X[V][2], P[V][2];
 #pragma unroll
@@ -399,17 +448,18 @@ __device__ __forceinline__ void tbs_pass(const TbArgs& a, const CUtensorMap* tm_
 #pragma unroll
             for (int j = 0; j < 2; ++j) P[v][j] = DMUL(coff, X[v][j]);
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(L::sempty());
         {
             const int wo = L::wr_off(warp, 0, st.hb, st.tc) + c0;
             tbs_sts2(wo, P[V - 2]);
             tbs_sts2(wo + RX, P[V - 1]);
             tbs_sts2(wo + 2 * RX, X[V - 1]);
+            TbsSync<C>::done_write(lane, 0, st);
         }
-        __syncwarp();
-        if (lane == 0) {
-            mbar_arrive(L::sempty());
-            mbar_arrive(L::hbar(st.hb & 1));
-        }
+        // warp 0 starts the next tile's copy once every warp has moved its rows of the
+        // x stage into registers (issuing it later, after the first hand-off round, which
+        // implies the same, measured 2% slower)
         if (warp == 0 && i + 1 < ntile) {
             mbar_wait(L::sempty(), st.tc & 1);  // the whole warp waits (no lone spinner)
             if (lane == 0) {
@@ -418,6 +468,7 @@ __device__ __forceinline__ void tbs_pass(const TbArgs& a, const CUtensorMap* tm_
             }
             __syncwarp();
         }
+        TBS_TICK(0);
         const int boff = C::OFF_B + (int)(st.tc & 1u) * C::BSTAGE + (warp * V + 5) * RX + c0;
         if (masked)
             tbs_dispatch<C, true>(h, X, P, om, coff, a.g.inv_diag, warp, lane, inmask, accmask, acc,
@@ -425,6 +476,7 @@ __device__ __forceinline__ void tbs_pass(const TbArgs& a, const CUtensorMap* tm_
         else
             tbs_dispatch<C, false>(h, X, P, om, coff, a.g.inv_diag, warp, lane, inmask, accmask,
                                    acc, st, boff);
+        TBS_TICK(32);
         st.hb += h;
         ++st.tc;
         // slot v now holds row R0 + v - h: mask bit v - h + 6
@@ -440,6 +492,17 @@ __device__ __forceinline__ void tbs_pass(const TbArgs& a, const CUtensorMap* tm_
                 }
             }
         }
+#ifdef SRJ_TBS_TIMING
+        if (blockIdx.x == 0 && st.tc == 3u && lane == 0 && (warp == 0 || warp == C::NW - 1)) {
+            const long long* tm = tbs_tm[warp != 0];
+            const long long t1 = clock64();
+            printf("warp %2d h %d: top->tma %lld  tma->pub0 %lld |", warp, h, tm[31] - tm[30], tm[0] - tm[31]);
+            for (int t = 0; t < h; ++t)
+                printf(" [int %lld wait %lld rest %lld]", tm[1 + 3 * t] - (t ? tm[3 * t] : tm[0]),
+                       tm[2 + 3 * t] - tm[1 + 3 * t], tm[3 + 3 * t] - tm[2 + 3 * t]);
+            printf(" | store %lld  tile %lld\n", t1 - tm[32], t1 - tm[30]);
+        }
+#endif
     }
 }
 

@@ -8,7 +8,8 @@ in orders a normal run never produces; mbarrier waits are bounded (a lost
 arrival traps instead of hanging); shared-memory and global index bounds are
 asserted in the staged kernels.  The parity tests below -- multi-tile grids
 with masked tiles, every rollback stop position, the speculative next-pass
-copy and its drain, the SOLVE and SLAB instantiations, the 1D register and
+copy and its drain, the SOLVE and SLAB instantiations, the skewed-tile 2D kernel
+(hand-off rounds, carry rows between tiles), the 1D register and
 shared-memory kernels, the batched collection kernel -- must stay bit-identical
 to the oracle under that build, several rounds each.  The negative control
 removes one wait (SRJ_STRESS_BREAK=1: the TB2D halo hand-off) and must fail.
@@ -50,6 +51,7 @@ SELECTION = [
     "tests/test_gpu_random_shapes.py::test_random_shape_cycle_bitwise[1d3var-4]",
     "tests/test_gpu_tbslabs.py::test_tb_slabs_graph_replay_matches_reference",
     "tests/test_gpu_var3d.py",
+    "tests/test_gpu_tbs.py",
 ]
 
 
