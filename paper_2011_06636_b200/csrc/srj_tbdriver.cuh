@@ -140,15 +140,34 @@ __device__ __forceinline__ TbCycleResult tb_cycle(const TbArgs& a, const int& M,
             issued = true;
         }
         reduce_partials_multi(part, nb, h, red);
+        // The reference's per-sweep checks (solver.py:216-222) for the h sub-sweeps at
+        // once: lane t of every warp evaluates sub-sweep t (one sqrt and one division
+        // instead of h in a row on every CTA's path to the next pass); the first lane
+        // that stops decides, as the sequential loop would.
         int stop_t = -1;
-        for (int t = 0; t < h; ++t) {
-            const int k = k0 + t;
-            if (k == 0) continue;  // res(x_0) is known to the host
-            r.S2 = red[t];
-            r.res = sqrt(r.S2) / a.baseline;
-            if (blockIdx.x == 0 && threadIdx.x == 0) hist[k] = r.res;
-            if (!isfinite(r.res)) { r.status = kStatusDiverged; stop_t = t; break; }
-            if (r.res <= a.tol) { r.status = kStatusConverged; stop_t = t; break; }
+        {
+            const int lane = threadIdx.x & 31;
+            const bool live = lane < h && k0 + lane != 0;  // res(x_0) is known to the host
+            const double S2l = live ? red[lane] : 0.0;
+            const double resl = sqrt(S2l) / a.baseline;
+            const bool bad = live && !isfinite(resl);
+            const bool conv = live && resl <= a.tol;
+            const unsigned stops = __ballot_sync(0xffffffffu, bad || conv);
+            const unsigned lives = __ballot_sync(0xffffffffu, live);
+            const int first = stops ? __ffs(stops) - 1 : h;
+            if (blockIdx.x == 0 && threadIdx.x < 32 && live && lane <= first) hist[k0 + lane] = resl;
+            const int src = stops ? first : (lives ? 31 - __clz(lives) : 0);
+            const double S2s = __shfl_sync(0xffffffffu, S2l, src);
+            const double ress = __shfl_sync(0xffffffffu, resl, src);
+            const bool bads = __shfl_sync(0xffffffffu, (int)bad, src) != 0;
+            if (lives) {
+                r.S2 = S2s;
+                r.res = ress;
+            }
+            if (stops) {
+                stop_t = first;
+                r.status = bads ? kStatusDiverged : kStatusConverged;
+            }
         }
         if (stop_t >= 0) {
             stopped = true;
