@@ -480,7 +480,9 @@ __global__ void __launch_bounds__(tb2d::Cfg<K>::THREADS, 1) __maxnreg__(tb2d::Cf
         tb2d_pass<K, SLAB>(a, tmx[in], &tm_b, xout, om, h, acc, accumulate, ownmask, phase, first,
                            na, hb, ne);
     };
-    auto issue = [&](int in) { tb2d_issue<K, SLAB>(a, tmx[in], &tm_b, blockIdx.x); };
+    auto issue = [&](int in) {  // a lane of the last warp (it has no part in the pass sums)
+        if (threadIdx.x == blockDim.x - 32) tb2d_issue<K, SLAB>(a, tmx[in], &tm_b, blockIdx.x);
+    };
     auto drain = [&]() __attribute__((always_inline)) {
         mbar_wait(L::bar(), phase);
         phase ^= 1u;

@@ -25,6 +25,17 @@
 #include "srj_tb.cuh"
 #include "srj_walk.cuh"
 
+#ifdef SRJ_TB_PHASETIME  // (tuning only) where the time between two passes goes
+#include <cstdio>
+#define TB_PT(k)                                                                  \
+    do {                                                                          \
+        if (threadIdx.x == 0 && p == 3 && (blockIdx.x == 0 || blockIdx.x == 70))  \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb_pt[k]));          \
+    } while (0)
+#else
+#define TB_PT(k) ((void)0)
+#endif
+
 namespace srj {
 
 struct TbArgs {
@@ -97,6 +108,14 @@ __device__ __forceinline__ TbCycleResult tb_cycle(const TbArgs& a, const int& M,
     const int npasses = (M + a.s - 1) / a.s;
     TbCycleResult r{M, kStatusRan, (cur + npasses) & 1, 0.0, 0.0};
     bool stopped = false, issued = false;
+    // fast stop test (see below): usable when sqrt(S2)/baseline cannot overflow
+    const double tolb = a.tol * a.baseline;
+    const double thr_hi = tolb * tolb * (1.0 + 1e-9);
+    const bool fast_ok = a.baseline >= 1e-150 && !(thr_hi != thr_hi);
+    int raw_to = 0;  // history entries 1 .. raw_to hold raw sums of squares
+#ifdef SRJ_TB_PHASETIME
+    unsigned long long tb_ph[8] = {};
+#endif
     for (int p = 0; p < npasses && !stopped; ++p) {
         const int k0 = p * a.s;
         const int h = min(a.s, M - k0);
@@ -104,7 +123,18 @@ __device__ __forceinline__ TbCycleResult tb_cycle(const TbArgs& a, const int& M,
         double acc[S];
 #pragma unroll
         for (int t = 0; t < S; ++t) acc[t] = 0.0;
+#ifdef SRJ_TB_PHASETIME
+        unsigned long long tb_pt[8];
+        if (threadIdx.x == 0 && p == 4 && (blockIdx.x == 0 || blockIdx.x == 70)) {
+            unsigned long long now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            printf("PH cta %d: tiles_end->sums %llu sums->gridbar %llu gridbar->reduce %llu reduce->stoptest %llu stoptest->nextpass %llu\n",
+                   (int)blockIdx.x, tb_ph[1] - tb_ph[0], tb_ph[2] - tb_ph[1], tb_ph[3] - tb_ph[2],
+                   tb_ph[4] - tb_ph[3], now - tb_ph[4]);
+        }
+#endif
         pass(in, buf[in ^ 1], omegas + k0, h, acc, true, issued);
+        TB_PT(0);
         issued = false;
         double* part = a.partials + (size_t)(phase++ & 1) * kTbMaxSub * nb;
         {
@@ -126,7 +156,9 @@ __device__ __forceinline__ TbCycleResult tb_cycle(const TbArgs& a, const int& M,
                 part[threadIdx.x * nb + blockIdx.x] = v;
             }
         }
+        TB_PT(1);
         grid_barrier();
+        TB_PT(2);
         if constexpr (SLAB) {  // pass mode: raw sums, no decision, no tail
             reduce_partials_multi(part, nb, h, red);
             if (blockIdx.x == 0 && threadIdx.x < h) a.sums[threadIdx.x] = red[threadIdx.x];
@@ -136,39 +168,45 @@ __device__ __forceinline__ TbCycleResult tb_cycle(const TbArgs& a, const int& M,
         }
         // Speculatively start the next pass's first tile while the stop test runs.
         if (p + 1 < npasses && has_tiles) {
-            if (threadIdx.x == 0) issue(in ^ 1);
+            issue(in ^ 1);  // every thread calls; the kernel picks the issuing thread
             issued = true;
         }
         reduce_partials_multi(part, nb, h, red);
+        TB_PT(3);
         // The reference's per-sweep checks (solver.py:216-222) for the h sub-sweeps at
-        // once: lane t of every warp evaluates sub-sweep t (one sqrt and one division
-        // instead of h in a row on every CTA's path to the next pass); the first lane
-        // that stops decides, as the sequential loop would.
+        // once: lane t of every warp evaluates sub-sweep t; the first lane that stops
+        // decides, as the sequential loop would.  Fast path: a sum of squares that is
+        // finite and above (tol*baseline)^2 by a margin far beyond the rounding of
+        // sqrt and the division cannot stop the cycle, so no sqrt / division sits on
+        // the path to the next pass; the history keeps the raw sums until the end of
+        // the cycle (hist_raw_to .. converted below).
         int stop_t = -1;
         {
             const int lane = threadIdx.x & 31;
             const bool live = lane < h && k0 + lane != 0;  // res(x_0) is known to the host
             const double S2l = live ? red[lane] : 0.0;
-            const double resl = sqrt(S2l) / a.baseline;
-            const bool bad = live && !isfinite(resl);
-            const bool conv = live && resl <= a.tol;
-            const unsigned stops = __ballot_sync(0xffffffffu, bad || conv);
-            const unsigned lives = __ballot_sync(0xffffffffu, live);
-            const int first = stops ? __ffs(stops) - 1 : h;
-            if (blockIdx.x == 0 && threadIdx.x < 32 && live && lane <= first) hist[k0 + lane] = resl;
-            const int src = stops ? first : (lives ? 31 - __clz(lives) : 0);
-            const double S2s = __shfl_sync(0xffffffffu, S2l, src);
-            const double ress = __shfl_sync(0xffffffffu, resl, src);
-            const bool bads = __shfl_sync(0xffffffffu, (int)bad, src) != 0;
-            if (lives) {
-                r.S2 = S2s;
-                r.res = ress;
-            }
-            if (stops) {
-                stop_t = first;
-                r.status = bads ? kStatusDiverged : kStatusConverged;
+            const bool sure = !live || (fast_ok && S2l > thr_hi && S2l < 1e290);
+            if (blockIdx.x == 0 && threadIdx.x < 32 && live) hist[k0 + lane] = S2l;  // raw
+            if (live) raw_to = k0 + lane;  // (lane-dependent; the maximum is taken below)
+            if (!__all_sync(0xffffffffu, sure)) {
+                const double resl = sqrt(S2l) / a.baseline;
+                const bool bad = live && !isfinite(resl);
+                const bool conv = live && resl <= a.tol;
+                const unsigned stops = __ballot_sync(0xffffffffu, bad || conv);
+                if (stops) {
+                    const int first = __ffs(stops) - 1;
+                    stop_t = first;
+                    r.S2 = __shfl_sync(0xffffffffu, S2l, first);
+                    r.res = __shfl_sync(0xffffffffu, resl, first);
+                    r.status = __shfl_sync(0xffffffffu, (int)bad, first) != 0 ? kStatusDiverged
+                                                                               : kStatusConverged;
+                }
             }
         }
+        TB_PT(4);
+#ifdef SRJ_TB_PHASETIME
+        if (p == 3) for (int k = 0; k < 8; ++k) tb_ph[k] = tb_pt[k];
+#endif
         if (stop_t >= 0) {
             stopped = true;
             r.executed = k0 + stop_t;
@@ -185,6 +223,17 @@ __device__ __forceinline__ TbCycleResult tb_cycle(const TbArgs& a, const int& M,
                 grid_barrier();
                 r.result = in ^ 1;
             }
+        }
+    }
+    if constexpr (!SLAB) {
+        // history: raw sums -> relative residuals (CTA 0; its own stores, made
+        // visible by the block barriers of the pass epilogue).  A stop at sub-sweep
+        // t leaves entries beyond k0+t that the host never reads (k > executed).
+        raw_to = __reduce_max_sync(0xffffffffu, raw_to);
+        if (blockIdx.x == 0) {
+            __syncthreads();
+            for (int k = 1 + (int)threadIdx.x; k <= raw_to; k += blockDim.x)
+                hist[k] = sqrt(hist[k]) / a.baseline;
         }
     }
     if (!stopped) {

@@ -37,7 +37,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
-#ifdef SRJ_TBS_TIMING
+#if defined(SRJ_TBS_TIMING) || defined(SRJ_TBS_PASSTIME)
 #include <cstdio>
 #endif
 #include <cstdlib>
@@ -399,6 +399,10 @@ __device__ __forceinline__ void tbs_pass(const TbArgs& a, const CUtensorMap* tm_
     const int nx = a.g.nx, ny = a.g.ny;
     const double coff = a.g.c_off;
     if (ntile == 0) return;
+#ifdef SRJ_TBS_PASSTIME
+    unsigned long long pt0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pt0));
+#endif
     // Pass start (every warp is past the previous pass's block barriers): the
     // pass's omegas into shared memory.
     if (threadIdx.x < h) L::om()[threadIdx.x] = __ldg(om + threadIdx.x);
@@ -410,7 +414,7 @@ __device__ __forceinline__ void tbs_pass(const TbArgs& a, const CUtensorMap* tm_
     const bool cown = lane >= S / 2 && lane < 32 - S / 2;  // region columns S .. RX-S-1
     for (int i = 0; i < ntile; ++i) {
         int R0, gx0, lo, hi;
-        bool masked;
+        bool masked, cin;
         unsigned inmask = 0u, ownmask = 0u;
         {
             const int4 d = L::desc(i);
@@ -419,21 +423,20 @@ __device__ __forceinline__ void tbs_pass(const TbArgs& a, const CUtensorMap* tm_
             R0 = d.y + warp * V;  // row of slot 0 at level 0
             gx0 = d.x - S + c0;
             // Over all levels a warp's slots hold rows R0-6 .. R0+4.  Fast path:
-            // every region column inside the grid and those rows all inside
-            // the segment (owned) or all outside it but inside the grid.
-            const bool colsok = d.x >= S && d.x + C::TX + S <= nx;
+            // those rows all inside the segment (owned) or all outside it but
+            // inside the grid.  Columns outside the grid (first / last strip)
+            // need no mask: a lane there relaxes with inv = 0, so its points stay
+            // at the zero the copy engine filled in (x' = 0 + w*(0*r), r finite:
+            // such a point has at most one non-zero neighbour product).
             const bool allown = R0 - 6 >= lo && R0 + 4 < hi;
             const bool noneown = (R0 + 4 < lo || R0 - 6 >= hi) && R0 - 6 >= 0 && R0 + 4 < ny;
-            masked = !(colsok && (allown || noneown));
-#ifdef SRJ_TBS_FORCEMASK  // (timing experiment: every warp takes the masked path)
-            masked = true;
-#endif
+            masked = !(allown || noneown);
+            cin = gx0 >= 0 && gx0 < nx;  // a lane's column pair is inside as a whole (even nx)
             if (masked) {
-                const bool cin = gx0 >= 0 && gx0 < nx;  // a lane's column pair is inside as a whole (even nx)
-                inmask = cin ? tbs_range_mask(6 - R0, ny + 6 - R0) : 0u;
+                inmask = tbs_range_mask(6 - R0, ny + 6 - R0);
                 ownmask = (cin && cown) ? tbs_range_mask(lo + 6 - R0, hi + 6 - R0) : 0u;
             } else {
-                ownmask = (allown && cown) ? 0x7ffu : 0u;
+                ownmask = (allown && cin && cown) ? 0x7ffu : 0u;
             }
         }
         const unsigned accmask = accumulate ? ownmask : 0u;
@@ -470,12 +473,11 @@ __device__ __forceinline__ void tbs_pass(const TbArgs& a, const CUtensorMap* tm_
         }
         TBS_TICK(0);
         const int boff = C::OFF_B + (int)(st.tc & 1u) * C::BSTAGE + (warp * V + 5) * RX + c0;
+        const double inv = cin ? a.g.inv_diag : 0.0;
         if (masked)
-            tbs_dispatch<C, true>(h, X, P, om, coff, a.g.inv_diag, warp, lane, inmask, accmask, acc,
-                                  st, boff);
+            tbs_dispatch<C, true>(h, X, P, om, coff, inv, warp, lane, inmask, accmask, acc, st, boff);
         else
-            tbs_dispatch<C, false>(h, X, P, om, coff, a.g.inv_diag, warp, lane, inmask, accmask,
-                                   acc, st, boff);
+            tbs_dispatch<C, false>(h, X, P, om, coff, inv, warp, lane, inmask, accmask, acc, st, boff);
         TBS_TICK(32);
         st.hb += h;
         ++st.tc;
@@ -504,6 +506,13 @@ __device__ __forceinline__ void tbs_pass(const TbArgs& a, const CUtensorMap* tm_
         }
 #endif
     }
+#ifdef SRJ_TBS_PASSTIME
+    if (st.tc == 4u * ntile && threadIdx.x == 0) {
+        unsigned long long pt1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pt1));
+        printf("PASS cta %d ntile %d start %llu dur %llu\n", (int)blockIdx.x, ntile, pt0, pt1 - pt0);
+    }
+#endif
 }
 
 template <class C, bool SOLVE>
@@ -543,9 +552,11 @@ __global__ void __launch_bounds__(C::THREADS, 1) __maxnreg__(C::MAXREG)
                     bool accumulate, bool first_issued) __attribute__((always_inline)) {
         tbs_pass<C>(a, tmx[in], &tm_b, xout, om, h, acc, accumulate, first_issued, ntile, st);
     };
-    auto issue = [&](int in) {
-        const int4 d = L::desc(0);
-        tbs_issue<C>(tmx[in], &tm_b, d.x, d.y, st.tc);
+    auto issue = [&](int in) {  // a lane of the last warp (it has no part in the pass sums)
+        if (threadIdx.x == blockDim.x - 32) {
+            const int4 d = L::desc(0);
+            tbs_issue<C>(tmx[in], &tm_b, d.x, d.y, st.tc);
+        }
     };
     auto drain = [&]() __attribute__((always_inline)) {
         mbar_wait(L::bar(), st.phase);

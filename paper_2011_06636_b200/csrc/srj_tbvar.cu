@@ -373,7 +373,9 @@ __global__ void __launch_bounds__(tbv::Cfg::THREADS, 1)
                     bool accumulate, bool first) __attribute__((always_inline)) {
         tbv_pass<SLAB>(a, tmx[in], m, xout, om, h, acc, accumulate, ownmask, phase, first, na, hb);
     };
-    auto issue = [&](int in) { tbv_issue<SLAB>(a, tmx[in], m, blockIdx.x); };
+    auto issue = [&](int in) {  // a lane of the last warp (it has no part in the pass sums)
+        if (threadIdx.x == blockDim.x - 32) tbv_issue<SLAB>(a, tmx[in], m, blockIdx.x);
+    };
     auto drain = [&]() __attribute__((always_inline)) {
         mbar_wait(L::bar(), phase);
         phase ^= 1u;

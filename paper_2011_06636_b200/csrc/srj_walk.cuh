@@ -62,8 +62,19 @@ __device__ __forceinline__ void grid_barrier() {
 // Sum of part[0..nb) in a fixed order; identical bits in every thread of
 // every CTA (all CTAs run the same code on the same data).
 __device__ __forceinline__ double reduce_partials(const double* part, int nb, double* sh) {
+    // four independent loads in flight per thread, added in ascending order (an
+    // absent entry adds +0)
     double s = 0.0;
-    for (int q = threadIdx.x; q < nb; q += blockDim.x) s += __ldcg(part + q);
+    for (int q0 = threadIdx.x; q0 < nb; q0 += 4 * blockDim.x) {
+        double v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int q = q0 + k * (int)blockDim.x;
+            v[k] = q < nb ? __ldcg(part + q) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) s += v[k];
+    }
     return block_allsum(s, sh);
 }
 
@@ -119,8 +130,20 @@ __device__ __forceinline__ void reduce_partials_multi(const double* part, int nb
                                                       double* out) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (wid < h) {
+        // Eight independent loads in flight per lane (one L2 round trip for up to
+        // 256 CTAs instead of one per 32), added in the same ascending order; an
+        // absent entry adds +0, which leaves a sum of squares unchanged.
         double s = 0.0;
-        for (int q = lane; q < nb; q += 32) s += __ldcg(part + wid * nb + q);
+        for (int q0 = 0; q0 < nb; q0 += 256) {
+            double v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int q = q0 + lane + 32 * k;
+                v[k] = q < nb ? __ldcg(part + wid * nb + q) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s += v[k];
+        }
         s = warp_allsum(s);
         if (lane == 0) out[wid] = s;
     }
