@@ -10,7 +10,8 @@
 // it held before, so level t of tile (oy) covers rows [oy - t, oy + RY - t).
 // New slot v of warp w is computed from old slots v-2 (south), v-1 (centre) and
 // v (north): every value a warp needs from below is its own, and the two rows
-// it needs from above come from the warp above (old slots V-2, V-1) -- or, for
+// it needs from above come from the warp above (x of its old slots V-2, V-1,
+// published in shared memory; the products are recomputed by the reader) -- or, for
 // warp 0, from the last warp of the PREVIOUS tile of the strip, which left
 // them in a carry buffer, one entry per level.  Consecutive tiles of a strip
 // therefore fit together without any redundant rows: per pass a strip computes
@@ -73,7 +74,7 @@ struct CfgT {
     static constexpr int MAXREG = MAXREG_RAW > 255 ? 255 : MAXREG_RAW;
     static constexpr int BROWS = RY + S;          // b rows staged per tile: [oy - S, oy + RY)
     static constexpr int XSTAGE = RX * RY, BSTAGE = RX * BROWS;
-    static constexpr int HSLOT = 3 * RX;          // one publication: p[V-2], p[V-1], x[V-1]
+    static constexpr int HSLOT = 2 * RX;          // one publication: x[V-2], x[V-1]
     static constexpr int HBUF = NW * HSLOT;       // one parity of the warp-to-warp rows
     static constexpr int CARRY = S * HSLOT;       // one tile parity of the tile-to-tile rows
     // shared-memory layout (doubles)
@@ -284,9 +285,14 @@ __device__ __forceinline__ void tbs_tile_sweeps(double (&X)[C::V][2], double (&P
         double p4[2], p5[2], x5[2];
         {
             const int ro = L::rd_off(warp, t, st.hb, st.tc) + c0;
-            tbs_lds2(p4, ro);
-            tbs_lds2(p5, ro + RX);
-            tbs_lds2(x5, ro + 2 * RX);
+            double x4[2];
+            tbs_lds2(x4, ro);
+            tbs_lds2(x5, ro + RX);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                p4[j] = DMUL(coff, x4[j]);
+                p5[j] = DMUL(coff, x5[j]);
+            }
         }
         {  // new slots 0, 1 (4 chains)
             const double p5w = shfl_up_d(p5[1], 1), p5e = shfl_down_d(p5[0], 1);
@@ -346,9 +352,8 @@ __device__ __forceinline__ void tbs_tile_sweeps(double (&X)[C::V][2], double (&P
 #pragma unroll
                 for (int j = 0; j < 2; ++j) P[v][j] = DMUL(coff, X[v][j]);
             const int wo = L::wr_off(warp, t + 1, st.hb, st.tc) + c0;
-            tbs_sts2(wo, P[V - 2]);
-            tbs_sts2(wo + RX, P[V - 1]);
-            tbs_sts2(wo + 2 * RX, X[V - 1]);
+            tbs_sts2(wo, X[V - 2]);
+            tbs_sts2(wo + RX, X[V - 1]);
             TbsSync<C>::done_write(lane, t + 1, st);
         }
         TBS_TICK(3 + 3 * t);
@@ -455,9 +460,8 @@ __device__ __forceinline__ void tbs_pass(const TbArgs& a, const CUtensorMap* tm_
         if (lane == 0) mbar_arrive(L::sempty());
         {
             const int wo = L::wr_off(warp, 0, st.hb, st.tc) + c0;
-            tbs_sts2(wo, P[V - 2]);
-            tbs_sts2(wo + RX, P[V - 1]);
-            tbs_sts2(wo + 2 * RX, X[V - 1]);
+            tbs_sts2(wo, X[V - 2]);
+            tbs_sts2(wo + RX, X[V - 1]);
             TbsSync<C>::done_write(lane, 0, st);
         }
         // warp 0 starts the next tile's copy once every warp has moved its rows of the
