@@ -25,17 +25,6 @@
 #include "srj_tb.cuh"
 #include "srj_walk.cuh"
 
-#ifdef SRJ_TB_PHASETIME  // (tuning only) where the time between two passes goes
-#include <cstdio>
-#define TB_PT(k)                                                                  \
-    do {                                                                          \
-        if (threadIdx.x == 0 && p == 3 && (blockIdx.x == 0 || blockIdx.x == 70))  \
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb_pt[k]));          \
-    } while (0)
-#else
-#define TB_PT(k) ((void)0)
-#endif
-
 namespace srj {
 
 struct TbArgs {
@@ -113,9 +102,6 @@ __device__ __forceinline__ TbCycleResult tb_cycle(const TbArgs& a, const int& M,
     const double thr_hi = tolb * tolb * (1.0 + 1e-9);
     const bool fast_ok = a.baseline >= 1e-150 && !(thr_hi != thr_hi);
     int raw_to = 0;  // history entries 1 .. raw_to hold raw sums of squares
-#ifdef SRJ_TB_PHASETIME
-    unsigned long long tb_ph[8] = {};
-#endif
     for (int p = 0; p < npasses && !stopped; ++p) {
         const int k0 = p * a.s;
         const int h = min(a.s, M - k0);
@@ -123,18 +109,7 @@ __device__ __forceinline__ TbCycleResult tb_cycle(const TbArgs& a, const int& M,
         double acc[S];
 #pragma unroll
         for (int t = 0; t < S; ++t) acc[t] = 0.0;
-#ifdef SRJ_TB_PHASETIME
-        unsigned long long tb_pt[8];
-        if (threadIdx.x == 0 && p == 4 && (blockIdx.x == 0 || blockIdx.x == 70)) {
-            unsigned long long now;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-            printf("PH cta %d: tiles_end->sums %llu sums->gridbar %llu gridbar->reduce %llu reduce->stoptest %llu stoptest->nextpass %llu\n",
-                   (int)blockIdx.x, tb_ph[1] - tb_ph[0], tb_ph[2] - tb_ph[1], tb_ph[3] - tb_ph[2],
-                   tb_ph[4] - tb_ph[3], now - tb_ph[4]);
-        }
-#endif
         pass(in, buf[in ^ 1], omegas + k0, h, acc, true, issued);
-        TB_PT(0);
         issued = false;
         double* part = a.partials + (size_t)(phase++ & 1) * kTbMaxSub * nb;
         {
@@ -156,9 +131,7 @@ __device__ __forceinline__ TbCycleResult tb_cycle(const TbArgs& a, const int& M,
                 part[threadIdx.x * nb + blockIdx.x] = v;
             }
         }
-        TB_PT(1);
         grid_barrier();
-        TB_PT(2);
         if constexpr (SLAB) {  // pass mode: raw sums, no decision, no tail
             reduce_partials_multi(part, nb, h, red);
             if (blockIdx.x == 0 && threadIdx.x < h) a.sums[threadIdx.x] = red[threadIdx.x];
@@ -172,7 +145,6 @@ __device__ __forceinline__ TbCycleResult tb_cycle(const TbArgs& a, const int& M,
             issued = true;
         }
         reduce_partials_multi(part, nb, h, red);
-        TB_PT(3);
         // The reference's per-sweep checks (solver.py:216-222) for the h sub-sweeps at
         // once: lane t of every warp evaluates sub-sweep t; the first lane that stops
         // decides, as the sequential loop would.  Fast path: a sum of squares that is
@@ -203,10 +175,6 @@ __device__ __forceinline__ TbCycleResult tb_cycle(const TbArgs& a, const int& M,
                 }
             }
         }
-        TB_PT(4);
-#ifdef SRJ_TB_PHASETIME
-        if (p == 3) for (int k = 0; k < 8; ++k) tb_ph[k] = tb_pt[k];
-#endif
         if (stop_t >= 0) {
             stopped = true;
             r.executed = k0 + stop_t;
