@@ -169,6 +169,19 @@ enum srj_tb_kind {
                                   kind; other values return SRJ_BAD_ARGUMENT     */
 };
 int srj_op_set_temporal_kernel(srj_op* op, int32_t kind);
+
+/* Work plan of the skewed-tile 2D kernel (SRJ_KERNEL_TBS2D) for an nx x ny grid
+ * on num_ctas CTAs, computed on the host (no CUDA call; diagnostics and tests).
+ * The grid is cut into strips of tile_cols owned columns; a strip's rows into
+ * segments [lo, hi); a segment into tiles of tile_rows rows starting `sweeps`
+ * rows above lo.  CTA c runs table[4*(c*tiles_per_cta + i)] = {ox, oy, lo, hi}
+ * for i = 0.. until an entry with hi <= lo.  `table` may be NULL (sizes only);
+ * `capacity` = ints it can hold (4 * num_ctas * tiles_per_cta needed, else
+ * SRJ_BAD_ARGUMENT).  There is no reference counterpart: the reference sweeps
+ * the whole vector at once (solver.py:225-233). */
+int srj_skew_plan(int64_t nx, int64_t ny, int32_t num_ctas, int32_t* tiles_per_cta,
+                  int32_t* ctas_used, int32_t* tile_rows, int32_t* tile_cols, int32_t* sweeps,
+                  int32_t* table, int64_t capacity);
 int srj_op_describe(const srj_op* op, srj_op_info* info);
 
 /* sum_i (b - A x)_i^2 -> *sumsq_host.  Synchronises `stream`. */

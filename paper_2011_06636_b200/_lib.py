@@ -29,7 +29,7 @@ EXPORTED_SYMBOLS = (
     "srj_run_cycle", "srj_sweep", "srj_matvec", "srj_fill_uniform_rhs",
     "srj_op_planes", "srj_sweep_planes", "srj_run_cycle_diffinf", "srj_batch_cycles_1d",
     "srj_op_set_temporal_kernel", "srj_tb_pass", "srj_op_solve_supported", "srj_solve",
-    "srj_op_set_reserved_sms",
+    "srj_op_set_reserved_sms", "srj_skew_plan",
     "srj_nccl_available", "srj_nccl_last_error", "srj_nccl_unique_id", "srj_nccl_comm_init",
     "srj_nccl_comm_destroy", "srj_slab_exchange", "srj_allgather_sums", "srj_slab_cycle_forward",
     "srj_slab_exchange_plan",
@@ -159,6 +159,32 @@ def _declare(L):
         if name not in ("srj_abi_version", "srj_last_error", "srj_nccl_last_error"):
             getattr(L, name).restype = c_int32
     L.srj_op_planes.restype = c_int64
+
+
+def skew_plan(nx: int, ny: int, num_ctas: int = 148):
+    """Work plan of the skewed-tile 2D kernel (srj_skew_plan; host only, no GPU
+    needed): dict with tiles_per_cta, ctas_used, tile_rows, tile_cols, sweeps
+    and `tiles`, one list of (ox, oy, lo, hi) per CTA."""
+    L = load()
+    T, used, rows, cols, sw = (c_int32() for _ in range(5))
+    byref = ctypes.byref
+    check(L.srj_skew_plan(c_int64(nx), c_int64(ny), c_int32(num_ctas), byref(T), byref(used),
+                          byref(rows), byref(cols), byref(sw), None, c_int64(0)), "srj_skew_plan")
+    n = 4 * num_ctas * T.value
+    table = (c_int32 * n)()
+    check(L.srj_skew_plan(c_int64(nx), c_int64(ny), c_int32(num_ctas), byref(T), byref(used),
+                          byref(rows), byref(cols), byref(sw), table, c_int64(n)), "srj_skew_plan")
+    tiles = []
+    for c in range(num_ctas):
+        mine = []
+        for i in range(T.value):
+            ox, oy, lo, hi = table[4 * (c * T.value + i):4 * (c * T.value + i) + 4]
+            if hi <= lo:
+                break
+            mine.append((ox, oy, lo, hi))
+        tiles.append(mine)
+    return {"tiles_per_cta": T.value, "ctas_used": used.value, "tile_rows": rows.value,
+            "tile_cols": cols.value, "sweeps": sw.value, "tiles": tiles}
 
 
 STRESS_LIB_PATH = os.path.join(_HERE, "libsrj_stress.so")

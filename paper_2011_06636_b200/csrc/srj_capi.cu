@@ -895,6 +895,22 @@ int srj_op_set_temporal_kernel(srj_op* op, int32_t kind) {
     return SRJ_OK;
 }
 
+int srj_skew_plan(int64_t nx, int64_t ny, int32_t num_ctas, int32_t* tiles_per_cta,
+                  int32_t* ctas_used, int32_t* tile_rows, int32_t* tile_cols, int32_t* sweeps,
+                  int32_t* table, int64_t capacity) {
+    if (nx < 1 || ny < 1 || nx >= (1ll << 30) || ny >= (1ll << 30) || num_ctas < 1 || num_ctas > 65536)
+        return fail(SRJ_BAD_ARGUMENT, "skew plan: extents or CTA count out of range");
+    int T = 0, used = 0;
+    if (tbs_plan_table((int)nx, (int)ny, num_ctas, table, capacity, &T, &used) != 0)
+        return fail(SRJ_BAD_ARGUMENT, "skew plan: table capacity too small");
+    if (tiles_per_cta) *tiles_per_cta = T;
+    if (ctas_used) *ctas_used = used;
+    if (tile_rows) *tile_rows = tbs_tile_rows();
+    if (tile_cols) *tile_cols = tbs_tile_cols();
+    if (sweeps) *sweeps = tbs_sweeps();
+    return SRJ_OK;
+}
+
 int srj_op_describe(const srj_op* op, srj_op_info* info) {
     if (!op || !info) return fail(SRJ_BAD_ARGUMENT, "null argument");
     info->num_sms = op->num_sms;

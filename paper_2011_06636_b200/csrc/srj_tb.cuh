@@ -33,6 +33,12 @@ cudaError_t tbs_plan_init(TbPlan& plan, const Geom& g, int num_sms);
 void tbs_plan_free(TbPlan& plan);
 cudaError_t tbs_launch_cycle(const TbPlan& plan, const Geom& g, TbArgs& a, double* x, double* x_alt,
                              const double* b, cudaStream_t st);
+// Host-side packing of the skewed tiles (no CUDA call; srj_skew_plan).  `tab` gets
+// ncta * T entries of 4 ints {ox, oy, lo, hi}.
+int tbs_plan_table(int nx, int ny, int ncta, int* tab, long long capacity, int* T, int* used);
+int tbs_tile_rows();
+int tbs_tile_cols();
+int tbs_sweeps();
 // True when a whole-grid launch at s sweeps per pass runs the skewed-tile kernel.
 bool tb_uses_skew(const TbPlan& plan, int s);
 

@@ -607,6 +607,35 @@ static bool tbs_pack(int nx, int ny, int ncta, int T, std::vector<int4>& tab, in
     return true;
 }
 
+// The smallest budget T of tiles per CTA that packs the grid into `ncta` CTAs,
+// with its table (ncta * T entries {ox, oy, lo, hi}, hi <= lo: no tile) and
+// the CTAs that own tiles.  Host only (no CUDA call): srj_skew_plan exposes it.
+void tbs_plan_tiles(int nx, int ny, int ncta, std::vector<int4>& tab, int& T, int& used) {
+    using C = tbs::Cfg;
+    const int strips = (nx + C::TX - 1) / C::TX;
+    const long long need = (long long)strips * (ny + 2 * C::S);
+    T = (int)std::max<long long>(1, (need + (long long)C::RY * ncta - 1) / ((long long)C::RY * ncta));
+    while (!tbs_pack(nx, ny, ncta, T, tab, used)) ++T;
+}
+
+int tbs_plan_table(int nx, int ny, int ncta, int* out, long long capacity, int* T, int* used) {
+    std::vector<int4> tab;
+    tbs_plan_tiles(nx, ny, ncta, tab, *T, *used);
+    if (out == nullptr) return 0;
+    if ((long long)tab.size() * 4 > capacity) return -1;
+    for (size_t i = 0; i < tab.size(); ++i) {
+        out[4 * i + 0] = tab[i].x;
+        out[4 * i + 1] = tab[i].y;
+        out[4 * i + 2] = tab[i].z;
+        out[4 * i + 3] = tab[i].w;
+    }
+    return 0;
+}
+
+int tbs_tile_rows() { return tbs::Cfg::RY; }
+int tbs_tile_cols() { return tbs::Cfg::TX; }
+int tbs_sweeps() { return tbs::Cfg::S; }
+
 cudaError_t tbs_plan_init(TbPlan& plan, const Geom& g, int num_sms) {
     using C = tbs::Cfg;
     plan.skew = false;
@@ -624,12 +653,9 @@ cudaError_t tbs_plan_init(TbPlan& plan, const Geom& g, int num_sms) {
                                                            C::SMEM)) != cudaSuccess)
         return e;
     if (occ < 1) return cudaSuccess;
-    const int strips = (g.nx + C::TX - 1) / C::TX;
-    const long long need = (long long)strips * (g.ny + 2 * C::S);
-    int T = (int)std::max<long long>(1, (need + (long long)C::RY * num_sms - 1) / ((long long)C::RY * num_sms));
     std::vector<int4> tab;
-    int used = 0;
-    while (!tbs_pack(g.nx, g.ny, num_sms, T, tab, used)) ++T;
+    int T = 0, used = 0;
+    tbs_plan_tiles(g.nx, g.ny, num_sms, tab, T, used);
     if (T > C::MAXT) return cudaSuccess;  // descriptors would not fit: square tiles serve the grid
     plan.skew_tpc = T;
     plan.skew_blocks = used;
