@@ -105,3 +105,62 @@ def test_tbs_golden_solves(name, device_loop, force_skew):
     rows = [(q.cycle, q.level, q.M, q.executed, q.residual_before, q.residual_after,
              q.average_rate) for q in rep.cycles]
     P.assert_trace_matches(c, rows, rep.total_iterations, rep.converged, x=rep.x.cpu().numpy())
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_tbs_random_shapes_bitwise(seed, force_skew):
+    """Random even-nx grids (strips with one to fourteen column pairs in the grid,
+    one to eight tiles per strip, segments cut at random places by the packing),
+    5 or 6 sweeps per pass, one random stop: bit for bit against oracle sweeps."""
+    import torch
+
+    import paper_2011_06636_b200 as srj
+    from oracle import srj_oracle as O
+    rng = np.random.default_rng(1000 + seed)
+    nx = 2 * int(rng.integers(1, 360))
+    ny = int(rng.integers(1, 720))
+    spp = int(rng.integers(5, 7))
+    M = int(rng.integers(7, 20))
+    dev = torch.device("cuda", 0)
+    dx2 = float(rng.uniform(1.0, 400.0))
+    A = srj.StencilOperator("2d5", (nx, ny), dx2=dx2, device=dev)
+    A.set_sweeps_per_pass(spp)
+    assert A.describe()["cycle_kernel"] == 11
+    op = O.StencilCPU("2d5", nx, ny, 1, dx2)
+    b = rng.uniform(-1, 1, A.n)
+    x0 = rng.uniform(-1, 1, A.n)
+    omegas = rng.uniform(0.4, 2.6, M)
+    baseline = 2.0
+    xs, res = _oracle_sweeps(op, x0, b, omegas, baseline)
+    om = torch.tensor(omegas, dtype=torch.float64, device=dev)
+    bf = A.field(b)
+    for stop in (None, int(rng.integers(1, M))):
+        tol = 0.0
+        if stop is not None:
+            tol = res[stop] * (1.0 + 1e-9)
+            if any(r <= tol * (1.0 + 1e-9) for r in res[:stop]):
+                continue
+        x, x_alt = A.field(x0), A.new_field()
+        hist = np.zeros(M)
+        out = A.run_cycle(x, x_alt, bf, om, M, tol, baseline, res[0], 10**9, hist)
+        k = M if stop is None else stop
+        assert out.executed == k, (nx, ny, spp, stop, out.executed)
+        got = (x_alt if out.result_in_alt else x).interior.cpu().numpy()
+        assert np.array_equal(got, xs[k]), (nx, ny, spp, stop, np.max(np.abs(got - xs[k])))
+        np.testing.assert_allclose(hist[:k], res[1:k + 1], rtol=1e-12)
+
+
+def test_skew_kernel_is_chosen_by_region_rows():
+    """Default choice (no override): the skewed tiles where they compute fewer
+    region rows per CTA and pass than the square ones -- 1024^2 and the C2 grid,
+    not 256^2 -- and never for <= 4 sweeps per pass."""
+    import torch
+
+    import paper_2011_06636_b200 as srj
+    assert "SRJ_TB_SKEW" not in os.environ
+    dev = torch.device("cuda", 0)
+    for n, want in ((256, 1), (1024, 11), (2048, 11)):
+        A = srj.StencilOperator("2d5", (n, n), device=dev)
+        assert A.describe()["cycle_kernel"] == want, (n, A.describe())
+        A.set_sweeps_per_pass(4)
+        assert A.describe()["cycle_kernel"] == 1
