@@ -19,14 +19,16 @@
 // owned).
 //
 // Segments.  148 CTAs need more parallelism than the strips offer, so a strip
-// is cut into segments of rows [lo, hi); a segment starts S rows early (tile
-// oy = lo - S) with whatever the carry buffers hold: the values that depend on
-// it (slots < 2t at level t) stay above row lo at every level, exactly like the
-// ring of a square tile, and are neither stored nor counted.  A segment costs
-// 2S extra rows, once (restart + skew), instead of 2S rows per tile.  The host
-// packs segments into equal budgets of T tiles per CTA (tbs_plan_init); at
-// 2048^2 a CTA runs 6 tiles of 96 rows where the square tiles need 10 rounds
-// of 72 region rows.
+// is cut into segments of rows [lo, hi); a segment inside the grid starts 2S rows
+// early (tile oy = lo - 2S) with whatever the carry buffers hold: the values that
+// depend on it (slots < 2t at level t) never reach slot 2S.  A cut moves up with
+// the level -- the segment below it owns row >= cut - t at level t -- so ownership
+// is a property of the slot (slot >= lo - oy, < hi - oy), cuts fall on multiples
+// of V rows, and a warp owns all of its points at every level or none: only the
+// grid's top and bottom rows need masks.  A segment costs 2S extra rows, once,
+// instead of 2S rows per tile.  The host packs segments into equal budgets of T
+// tiles per CTA (tbs_plan_init); at 2048^2 a CTA runs 6 tiles of 96 rows where
+// the square tiles need 10 rounds of 72 region rows.
 //
 // b is read from the staged box every sub-sweep (the rows a thread needs move
 // up with the skew), which takes it out of the registers; that makes room for
@@ -262,7 +264,7 @@ __device__ __forceinline__ void tbs_tile_sweeps(double (&X)[C::V][2], double (&P
 #pragma unroll
     for (int t = 0; t < H; ++t) {
         const double w = L::om()[t];
-        const unsigned im = inmask >> (5 - t), am = accmask >> (5 - t);
+        const unsigned im = inmask >> (5 - t), am = im & accmask;
         double pw[V], pe[V];  // p across the lane boundary of the centre rows (old slots 0..V-2)
 #pragma unroll
         for (int v = 1; v < V - 1; ++v) {
@@ -427,22 +429,27 @@ __device__ __forceinline__ void tbs_pass(const TbArgs& a, const CUtensorMap* tm_
             hi = d.w;
             R0 = d.y + warp * V;  // row of slot 0 at level 0
             gx0 = d.x - S + c0;
-            // Over all levels a warp's slots hold rows R0-6 .. R0+4.  Fast path:
-            // those rows all inside the segment (owned) or all outside it but
-            // inside the grid.  Columns outside the grid (first / last strip)
-            // need no mask: a lane there relaxes with inv = 0, so its points stay
-            // at the zero the copy engine filled in (x' = 0 + w*(0*r), r finite:
-            // such a point has at most one non-zero neighbour product).
-            const bool allown = R0 - 6 >= lo && R0 + 4 < hi;
-            const bool noneown = (R0 + 4 < lo || R0 - 6 >= hi) && R0 - 6 >= 0 && R0 + 4 < ny;
-            masked = !(allown || noneown);
+            // Ownership.  Inside the grid a segment boundary moves up with the level
+            // (the pair (row, level t) belongs to the segment below the cut iff
+            // row >= cut - t - 1 for residuals, cut - t for values), which makes it a
+            // property of the SLOT: slot s = V*warp + v of the tile at oy is owned iff
+            // lo - oy <= s < hi - oy; the packing cuts at multiples of V rows and
+            // starts a segment 2S rows early, so a warp owns all of its slots or
+            // none.  At the grid's top and bottom ownership is "inside the grid",
+            // row by row and level by level (inmask).  Over all levels a warp's slots
+            // hold rows R0-6 .. R0+4: a warp with all of them inside the grid runs
+            // the unmasked code.  Columns outside the grid (first / last strip) need
+            // no mask: a lane there relaxes with inv = 0, so its points stay at the
+            // zero the copy engine filled in (x' = 0 + w*(0*r), r finite: such a
+            // point has at most one non-zero neighbour product).
+            const int s_lo = lo > 0 ? lo - d.y : 0, s_hi = hi < ny ? hi - d.y : C::RY;
+            const int a0 = min(max(s_lo - warp * V, 0), V), a1 = min(max(s_hi - warp * V, 0), V);
+            const unsigned slots = a1 > a0 ? ((1u << a1) - 1u) & ~((1u << a0) - 1u) : 0u;
+            const bool allin = R0 - 6 >= 0 && R0 + 4 < ny;
+            masked = !(allin && (slots == 0u || slots == (1u << V) - 1u));
             cin = gx0 >= 0 && gx0 < nx;  // a lane's column pair is inside as a whole (even nx)
-            if (masked) {
-                inmask = tbs_range_mask(6 - R0, ny + 6 - R0);
-                ownmask = (cin && cown) ? tbs_range_mask(lo + 6 - R0, hi + 6 - R0) : 0u;
-            } else {
-                ownmask = (allown && cin && cown) ? 0x7ffu : 0u;
-            }
+            inmask = masked ? tbs_range_mask(6 - R0, ny + 6 - R0) : 0x7ffu;
+            ownmask = (cin && cown) ? slots : 0u;
         }
         const unsigned accmask = accumulate ? ownmask : 0u;
         TBS_TICK(30);
@@ -485,8 +492,8 @@ __device__ __forceinline__ void tbs_pass(const TbArgs& a, const CUtensorMap* tm_
         TBS_TICK(32);
         st.hb += h;
         ++st.tc;
-        // slot v now holds row R0 + v - h: mask bit v - h + 6
-        const unsigned sm = ownmask >> (6 - h);
+        // slot v now holds row R0 + v - h (in-grid bit v - h + 6), owned by slot
+        const unsigned sm = (inmask >> (6 - h)) & ownmask;
         if (sm) {
 #pragma unroll
             for (int v = 0; v < V; ++v) {
@@ -589,12 +596,25 @@ static bool tbs_pack(int nx, int ny, int ncta, int T, std::vector<int4>& tab, in
         int pos = 0;
         while (pos < ny) {
             if (c >= ncta) return false;
-            const int cap = left * C::RY - 2 * C::S;
-            const int rows = std::min(cap, ny - pos);
-            const int k = (rows + 2 * C::S + C::RY - 1) / C::RY;
+            // lead: rows the first tile starts above the segment (a restart inside the
+            // grid: two warps of slots that only feed the skew; at the grid top: the skew)
+            const int lead = pos > 0 ? 2 * C::S : C::S;
+            int rows, k;
+            if (ny - pos + lead + C::S <= left * C::RY) {  // to the grid's bottom (skew: S rows)
+                rows = ny - pos;
+                k = (rows + lead + C::S + C::RY - 1) / C::RY;
+            } else {  // cut inside the grid, at a multiple of V rows (whole warps own or not)
+                rows = std::min((left * C::RY - lead) / C::V * C::V, (ny - pos - 1) / C::V * C::V);
+                k = (rows + lead + C::RY - 1) / C::RY;
+                if (rows <= 0) {  // (budget too small for a cut here: next CTA)
+                    ++c;
+                    left = T;
+                    continue;
+                }
+            }
             for (int i = 0; i < k; ++i)
                 tab[(size_t)c * T + (T - left) + i] =
-                    make_int4(sx * C::TX, pos - C::S + i * C::RY, pos, pos + rows);
+                    make_int4(sx * C::TX, pos - lead + i * C::RY, pos, pos + rows);
             left -= k;
             pos += rows;
             if (left == 0) {
@@ -613,7 +633,7 @@ static bool tbs_pack(int nx, int ny, int ncta, int T, std::vector<int4>& tab, in
 void tbs_plan_tiles(int nx, int ny, int ncta, std::vector<int4>& tab, int& T, int& used) {
     using C = tbs::Cfg;
     const int strips = (nx + C::TX - 1) / C::TX;
-    const long long need = (long long)strips * (ny + 2 * C::S);
+    const long long need = (long long)strips * (ny + 2 * C::S);  // one segment per strip
     T = (int)std::max<long long>(1, (need + (long long)C::RY * ncta - 1) / ((long long)C::RY * ncta));
     while (!tbs_pack(nx, ny, ncta, T, tab, used)) ++T;
 }

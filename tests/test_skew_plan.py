@@ -1,8 +1,10 @@
 """Host-side work plan of the skewed-tile 2D kernel (srj_skew_plan, CPU only).
 
 The kernel trusts the table: every grid row of every strip must be owned by
-exactly one segment, a segment's tiles must start `sweeps` rows above it and
-follow each other every tile_rows rows until they cover it at every level, a
+exactly one segment, a segment's tiles must start 2 * sweeps rows above it
+(sweeps at the grid's top) and follow each other every tile_rows rows until
+their slots cover it (plus the skew at the grid's bottom), cuts inside the
+grid must fall on multiples of the rows per warp, a
 CTA's tiles of one segment must be consecutive (the carry rows go from one
 tile to the next), and no CTA may exceed the budget.
 """
@@ -39,8 +41,13 @@ def test_plan_covers_every_row_once(nx, ny, ncta):
             ox, oy, lo, hi = tiles[i]
             assert ox % TX == 0 and 0 <= ox < nx
             assert 0 <= lo < hi <= ny
-            assert oy == lo - S  # a segment starts S rows early
-            k = -(-(hi - lo + 2 * S) // RY)  # tiles that cover the segment at every level
+            lead = 2 * S if lo > 0 else S  # restart inside the grid: 2S rows early; top: S
+            assert oy == lo - lead
+            if hi < ny:  # cut inside the grid: whole warps (V = S rows) own or not
+                assert (hi - lo) % S == 0
+                k = -(-(hi - lo + lead) // RY)
+            else:        # to the grid's bottom: S more rows of skew
+                k = -(-(hi - lo + lead + S) // RY)
             seg = tiles[i:i + k]
             assert len(seg) == k, "a segment's tiles stay on one CTA"
             for j, t in enumerate(seg):
@@ -63,7 +70,7 @@ def test_plan_budget_is_tight():
     assert (p["tiles_per_cta"], p["tile_rows"], p["tile_cols"], p["sweeps"]) == (6, 96, 52, 6)
     assert p["ctas_used"] == 147
     total = sum(len(t) for t in p["tiles"])
-    assert total == 880
+    assert total == 880, total
     for nx, ny, ncta in SHAPES:
         q = _lib.skew_plan(nx, ny, ncta)
         T, RY, TX, S = q["tiles_per_cta"], q["tile_rows"], q["tile_cols"], q["sweeps"]
