@@ -499,7 +499,9 @@ __device__ __forceinline__ void tbs_pass(const TbArgs& a, const CUtensorMap* tm_
             for (int v = 0; v < V; ++v) {
                 if ((sm >> v) & 1u) {
                     const int gy = R0 + v - h;
-                    SRJ_ASSERT(gy >= lo && gy < hi && gy >= 0 && gy < ny && gx0 >= 0 && gx0 + 1 < nx);
+                    // the segment's rows at level h: cuts inside the grid have moved up by h
+                    SRJ_ASSERT(gy >= (lo > 0 ? lo - h : 0) && gy < (hi < ny ? hi - h : ny) && gy >= 0 &&
+                               gy < ny && gx0 >= 0 && gx0 + 1 < nx);
                     *reinterpret_cast<double2*>(xout + (long long)gy * nx + gx0) =
                         make_double2(X[v][0], X[v][1]);
                 }
