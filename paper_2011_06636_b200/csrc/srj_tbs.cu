@@ -245,11 +245,13 @@ __device__ __forceinline__ void tbs_rows(const double (&X)[C::V][2], const doubl
 
 // H sub-sweeps (compile time) of the skewed tile held in registers: X, P are
 // the thread's V x 2 values and products at level 0 on entry, level H on exit
-// (slot v then holds row R0 + v - H).  MASKED warps (rows or columns partly
-// outside the grid or the segment): inmask / accmask, bit i <-> row offset
-// i - 6 from R0 with this thread's column pair folded in; the bit of new slot
-// v at sub-sweep t is v - t + 5.  Other warps own all of their points or none
-// (`accmask` != 0: all).  boff: this thread's offset into the b stage,
+// (slot v then holds row R0 + v - H).  MASKED warps (some row outside the grid
+// at some level: the grid's top and bottom): inmask, bit i <-> row offset i - 6
+// from R0 is inside the grid (the bit of new slot v at sub-sweep t is
+// v - t + 5); a row outside is held at 0 and not counted.  accmask: the slots
+// this thread owns (bit v; its column pair and `accumulate` folded in) -- all
+// or none in the other warps (`accmask` != 0: all), which count and keep every
+// point they compute.  boff: this thread's offset into the b stage,
 // stb + (V*warp + 5)*RX + c0; the row of new slot v at sub-sweep t sits
 // (v - t) rows further.
 template <class C, int H, bool MASKED>
